@@ -1,0 +1,325 @@
+"""Benchmark: batched temporal-stereo frame steps on B200 (config 5 shape).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+Workload (BASELINE.json config 5, the batched-sequence config at the
+config-2 shape): per GPU, B independent seeded sequences of 1242x375 uint8
+stereo pairs, D = 128 (d_max = 127), default SgmParams / PredictionParams,
+rendered on the device by the restated ray caster (ground slab, 8 boxes at
+5-60 m, far wall; forward 1 m/frame + noise, yaw/pitch/roll noise).  A step
+advances every sequence by one frame: warp + Kalman predict, hole fill,
+intervals, ragged SAD, 8-path SGM, WTA + variance, LR + SAD checks, Kalman
+update.  Frame 0 of each sequence is full range and runs in the warm-up;
+timed steps are predicted frames.  Multi-GPU: one process per GPU, each
+with its own B sequences (weak scaling, no inter-GPU traffic).
+
+value      frames/s over all ranks, inputs resident in HBM (device pointers)
+e2e        the same through the public API (BatchedPipeline.process_frames)
+           with pinned host images copied in and the fused left disparity
+           (KITTI uint16) of every sequence copied out each step
+roofline   aggregation stage (4 SGM family launches): algorithmic bytes
+           4*N_v + 8*HW per view / CUDA-event stage time
+cpu_baseline  the numpy oracle port on the host, one predicted frame per
+           process, P processes in parallel
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import multiprocessing as mp
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+H, W, D_MAX = 375, 1242, 127
+RIG = dict(f=718.9, b=0.54, cx=607.0, cy=185.0, width=W, height=H, d_max=D_MAX)
+SEQ_FRAMES = 50
+TEXTURE_SCALE = 0.05
+KERNELS_PER_STEP = 12   # zmax, zidx, fill_h, fill_v, cost, 4 x sgm, wta, fuse, any_valid
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- inputs
+
+def sequence_specs(n, seed0):
+    from paper_1708_06301_b200 import scenes
+    return [scenes.sequence_spec(seed=seed0 + s, n_frames=SEQ_FRAMES) for s in range(n)]
+
+
+def render_frames(specs, frames, device):
+    """Device images [len(frames)][B][2][H][W] (torch uint8)."""
+    import torch
+    from paper_1708_06301_b200 import _lib
+    from paper_1708_06301_b200.core import StereoRig
+    rig = _lib.rig_struct(StereoRig(**RIG))
+    B = len(specs)
+    n_box = specs[0][0].shape[0]
+    boxes = np.ascontiguousarray(np.stack([sp[0] for sp in specs]), np.float64)
+    seeds = np.arange(B, dtype=np.int64) + 17
+    out = torch.empty((len(frames), B, 2, H, W), dtype=torch.uint8, device=device)
+    stream = torch.cuda.current_stream(device).cuda_stream
+    for i, k in enumerate(frames):
+        poses = np.ascontiguousarray(np.stack([sp[1][k % SEQ_FRAMES] for sp in specs]), np.float64)
+        _lib.call("es_render", ctypes.byref(rig), _lib.ptr(boxes), n_box, _lib.ptr(poses),
+                  _lib.ptr(seeds), B, ctypes.c_double(TEXTURE_SCALE), 12,
+                  ctypes.c_void_p(out[i].data_ptr()), None, ctypes.c_void_p(stream))
+    torch.cuda.synchronize(device)
+    return out
+
+
+def motions_for(specs, k):
+    return [sp[2][k % SEQ_FRAMES] for sp in specs]
+
+
+# ----------------------------------------------------------------- clocks
+
+class Clocks:
+    def __init__(self, index):
+        self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}.csv")
+        q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- CPU port
+
+def _cpu_worker(args):
+    left0, right0, left1, right1, motion = args
+    import oracle as O
+    orc = O.OracleStereo(RIG["f"], RIG["b"], RIG["cx"], RIG["cy"], W, H, D_MAX)
+    orc.step(left0, right0, None)
+    t0 = time.perf_counter()
+    orc.step(left1, right1, motion)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(imgs0, imgs1, motions, procs):
+    """numpy oracle port: P processes, each one full-range warm frame (not
+    timed) then one timed predicted frame of its own sequence."""
+    P = min(procs, len(motions))
+    jobs = [(imgs0[s, 0], imgs0[s, 1], imgs1[s, 0], imgs1[s, 1], motions[s]) for s in range(P)]
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(P) as pool:
+        per = pool.map(_cpu_worker, jobs)
+    wall = time.perf_counter() - t0
+    fps = P / max(per)
+    return {"value": fps, "unit": "frames/s", "cores": P, "kind": "port",
+            "sample": f"{P} sequences x 1 predicted frame (1242x375, D=128) in {P} parallel "
+                      f"processes; per-frame {min(per):.1f}-{max(per):.1f} s; wall {wall:.0f} s "
+                      "incl. the untimed full-range frame"}
+
+
+# ----------------------------------------------------------------- main
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=32, help="sequences per GPU")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-procs", type=int, default=min(8, os.cpu_count() or 1))
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    import torch
+    import torch.distributed as dist
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+
+    K, Wm, B = args.steps, max(args.warmup, 3), args.batch
+    if Wm + K > SEQ_FRAMES:
+        raise SystemExit(f"warmup + steps must be <= {SEQ_FRAMES} (sequence length)")
+    config = {"workload": "config5: B independent 1242x375 sequences per GPU, D=128, "
+                          "8 paths, predicted frames (frame 0 full range in warm-up)",
+              "batch_per_gpu": B, "height": H, "width": W, "d_max": D_MAX,
+              "l2": "working set per step (ragged volumes of all sequences) >> 126 MB L2"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        specs = sequence_specs(args.cpu_procs, seed0=5000)
+        imgs = render_frames(specs, [0, 1], device).cpu().numpy()
+        motions = motions_for(specs, 1)
+        cb = cpu_baseline(imgs[0], imgs[1], motions, args.cpu_procs)
+        print(json.dumps({
+            "impl": "reference", "metric": "frames/s", "value": cb["value"], "unit": "frames/s",
+            "n_gpus": args.gpus, "steps": K, "warmup": Wm, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u16+f64", "data": "synthetic",
+            "config": config, "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}))
+        return
+
+    from paper_1708_06301_b200 import _lib, pipeline
+    from paper_1708_06301_b200.core import StereoRig
+
+    rig = StereoRig(**RIG)
+    specs = sequence_specs(B, seed0=1000 + 1000 * rank)
+    frames = list(range(Wm + K))
+    imgs = render_frames(specs, frames, device)
+    bp = pipeline.BatchedPipeline(rig, B, device=local)
+    eng = bp.engine
+    ext = torch.cuda.ExternalStream(eng.stream(), device=device)
+
+    # warm-up: frame 0 (full range) .. Wm-1, synced so have_state is known
+    for k in range(Wm):
+        bp.process_frames(None, motions_for(specs, k), sync=True, images_dev=imgs[k].data_ptr())
+
+    # ---- device-resident timed region ---------------------------------
+    _lib.call("es_ctx_profile", eng._h, 1)
+    clocks = Clocks(local) if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(ext):
+        ev0.record()
+    cells = 0
+    for i in range(K):
+        k = Wm + i
+        bp.process_frames(None, motions_for(specs, k), sync=False,
+                          images_dev=imgs[k].data_ptr())
+    with torch.cuda.stream(ext):
+        ev1.record()
+    bp.sync()
+    torch.cuda.synchronize(device)
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop() if clocks else None
+    stage = np.zeros(6)
+    nsteps = ctypes.c_int64()
+    _lib.call("es_ctx_stage_times", eng._h, _lib.ptr(stage), ctypes.byref(nsteps))
+    _lib.call("es_ctx_profile", eng._h, 0)
+    # cells of the last timed step (per view) for the byte model
+    for s in range(B):
+        l, r = eng.cells(s)
+        cells += l + r
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    frames_total = B * K * world
+    value = frames_total / (ms_max / 1e3)
+
+    # ---- end-to-end through the public API with host buffers ------------
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((B, 2, H, W), dtype=torch.uint8, pin_memory=True)
+        out_k = np.empty((H, W), np.uint16)
+        # restart the sequences so e2e runs the same frames
+        bp.reset()
+        for k in range(Wm):
+            host.copy_(imgs[k])
+            bp.process_frames(host.numpy(), motions_for(specs, k), sync=True)
+        staged = [imgs[Wm + i].cpu().pin_memory() for i in range(K)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(ext):
+            e0.record()
+        for i in range(K):
+            bp.process_frames(staged[i].numpy(), motions_for(specs, Wm + i), sync=True)
+            for s in range(B):
+                _lib.call("es_ctx_export", eng._h, _lib.ES_FUSED_KITTI, s, 0, _lib.ptr(out_k))
+        with torch.cuda.stream(ext):
+            e1.record()
+        torch.cuda.synchronize(device)
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": frames_total / (float(te.item()) / 1e3), "unit": "frames/s",
+               "h2d_bytes_per_step": int(B * 2 * H * W), "d2h_bytes_per_step": int(B * H * W * 2)}
+
+    # ---- roofline of the dominant kernel (aggregation stage) ------------
+    peak, peak_kind = peaks()
+    agg_ms = stage[3] / max(nsteps.value, 1)
+    hw = H * W
+    agg_bytes = 4 * cells + 8 * hw * 2 * B
+    achieved = agg_bytes / (agg_ms / 1e3) / 1e9
+    frame_bytes = 8 * cells + 106 * hw * 2 * B
+    stage_names = ["predict", "intervals", "cost", "aggregate", "wta_variance", "checks_fuse"]
+    line = {
+        "metric": "frames/s", "value": value, "unit": "frames/s", "n_gpus": world,
+        "steps": K, "warmup": Wm, "ms_per_step": ms_max / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u16+f64", "data": "synthetic",
+        "config": config,
+        "mde_per_s": value * hw * (D_MAX + 1) / 1e6,
+        "searched_mcells_per_s": cells * world / (ms_max / K / 1e3) / 1e6,
+        "search_fraction": cells / (2 * B * hw * (D_MAX + 1)),
+        "stage_ms_per_step": {n: stage[i] / max(nsteps.value, 1) for i, n in enumerate(stage_names)},
+        "roofline": {"bound": "hbm", "kernel": "sgm aggregation (4 family launches)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "bytes_per_step": agg_bytes},
+        "pipeline_roofline": {"achieved": frame_bytes / (ms_max / K / 1e3) / 1e9,
+                              "frac": frame_bytes / (ms_max / K / 1e3) / 1e9 / peak},
+        "gpu_launches": KERNELS_PER_STEP * K,
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        specs_c = sequence_specs(args.cpu_procs, seed0=1000)
+        imgs_c = render_frames(specs_c, [0, 1], device).cpu().numpy()
+        line["cpu_baseline"] = cpu_baseline(imgs_c[0], imgs_c[1], motions_for(specs_c, 1),
+                                            args.cpu_procs)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,124 @@
+// Common device types and helpers for the egostereo B200 hot path.
+//
+// Data layout in HBM (per sequence s, view v; "sv" = 2*s + v):
+//   images      uint8  [B][2][H][W]               (left = 0, right = 1)
+//   state d, p  f64    [B][2][H][W], valid uint8   (double-buffered)
+//   meta        uint2  [B][2][H][W]  .x = lo | hi << 16, .y = pair offset
+//   volumes     u16    pairs [B][2][H][rowcap]     (rowcap = W * npairs_max)
+// A pixel's interval [lo, hi] is stored as whole u16 pairs j = lo>>1 .. hi>>1
+// (pair j holds d = 2j, 2j+1), row-ragged: each image row owns a fixed
+// window of rowcap pairs and packs its pixels' pairs contiguously inside it.
+// Halves outside [lo, hi] hold the U16 "infinity" 0x8000.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace es {
+
+constexpr uint32_t INF16 = 0x8000u;            // u16 +inf sentinel
+constexpr uint32_t INF16x2 = 0x80008000u;
+constexpr uint32_t NO_SRC = 0xFFFFFFFFu;
+
+struct Rig {
+  double f, b, cx, cy;
+  int W, H, d_max;
+};
+
+struct Params {
+  int window;
+  float p1, p2;          // float32 penalties (numpy float32 arithmetic)
+  uint32_t p1i, p2i;     // integer penalties for the u16 path
+  double s_max, r_min, tau_lr, tau_sad;
+  double q, gamma_f, gamma_e;
+  int edge_window, edge_reject, fill_holes;
+  double p_init;
+};
+
+// error bits (per sequence)
+constexpr int ERR_POINT_AT_INFINITY = 1;
+constexpr int ERR_NONPOSITIVE_D = 2;
+
+__host__ __device__ inline int npairs_max(int d_max) { return (d_max >> 1) + 1; }
+
+__device__ __forceinline__ uint32_t lo_of(uint2 m) { return m.x & 0xFFFFu; }
+__device__ __forceinline__ uint32_t hi_of(uint2 m) { return m.x >> 16; }
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
+
+// numpy's float64 -> int64 conversion of floor/ceil/rint results on x86:
+// out-of-range and NaN become INT64_MIN.
+__device__ __forceinline__ long long np_to_i64(double v) {
+  if (!(v >= -9.2233720368547758e18 && v < 9.2233720368547758e18)) return (long long)0x8000000000000000ULL;
+  return (long long)v;
+}
+
+// Warp a pixel through a disparity-space homography exactly as the oracle
+// does (geometry.py:95-159): explicit k = 0..3 dot products, no FMA (the
+// translation unit is compiled with -fmad=false).  Returns false when the
+// fourth homogeneous component vanishes (PointAtInfinityError).
+__device__ __forceinline__ bool warp_point(const double* __restrict__ Hm, double x, double y,
+                                           double d, double cx, double cy, double& xp,
+                                           double& yp, double& dp) {
+  double px = x - cx, py = y - cy;
+  double o[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+    o[r] = ((Hm[4 * r + 0] * px + Hm[4 * r + 1] * py) + Hm[4 * r + 2] * d) + Hm[4 * r + 3];
+  if (fabs(o[3]) < 1e-12) return false;
+  xp = o[0] / o[3] + cx;
+  yp = o[1] / o[3] + cy;
+  dp = o[2] / o[3];
+  return true;
+}
+
+// widen/clamp an interval exactly as sgm.py:114-126
+__device__ __forceinline__ void interval_of(double d, double p, bool valid, int d_max, int& lo,
+                                            int& hi) {
+  if (!valid) {
+    lo = 0;
+    hi = d_max;
+    return;
+  }
+  const double s3 = 3.0 * sqrt(fmax(p, 0.0));
+  long long l = np_to_i64(floor(d - s3));
+  long long h = np_to_i64(ceil(d + s3));
+  l = l < 0 ? 0 : (l > d_max ? d_max : l);
+  h = h < 0 ? 0 : (h > d_max ? d_max : h);
+  for (int k = 0; k < 2; ++k) {
+    if ((h - l) < 2 && l > 0) --l;
+    if ((h - l) < 2 && h < d_max) ++h;
+  }
+  lo = (int)l;
+  hi = (int)h;
+}
+
+// block-wide exclusive scan of one uint32 per thread (blockDim.x <= 1024)
+template <int NT>
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* smem32,
+                                                         uint32_t& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem32[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t w = lane < NT / 32 ? smem32[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < NT / 32) smem32[lane] = w;
+  }
+  __syncthreads();
+  uint32_t base = wid ? smem32[wid - 1] : 0u;
+  total = smem32[NT / 32 - 1];
+  __syncthreads();
+  return base + x - v;
+}
+
+}  // namespace es

@@ -1,0 +1,281 @@
+// K1 + K2: forward warp with a deterministic two-phase z-buffer, Kalman
+// predict of the variance, zoom-hole fill, search intervals and the
+// row-ragged pair offsets.
+//
+// Reference: prediction.py:50-183, geometry.py:95-159, sgm.py:95-127.
+//
+// z-buffer (prediction.py:113-121): the surviving source of a target pixel
+// is the one with the largest warped disparity d', ties to the smallest
+// row-major source index.  Phase 1 (k_warp_zmax) takes atomicMax over the
+// IEEE bits of d' (> 0, so bit order == numeric order); phase 2
+// (k_warp_zidx) takes atomicMin over the source index among sources whose
+// d' equals the phase-1 maximum.  Every kernel that needs a source's warped
+// values recomputes them with the same code, so results are identical to a
+// serial row-major splat regardless of scheduling.
+#include "es_common.cuh"
+#include "es_kernels.h"
+
+namespace es {
+
+// edge test (prediction.py:50-64): valid pixel whose valid-neighbour
+// disparity range over the (2r+1)^2 window exceeds gamma_e
+__device__ __forceinline__ bool is_edge(const double* __restrict__ d, const uint8_t* __restrict__ v,
+                                        int x, int y, int W, int H, int r, double gamma_e) {
+  double hi = -INFINITY, lo = INFINITY;
+  for (int oy = -r; oy <= r; ++oy) {
+    int yy = y + oy;
+    if (yy < 0 || yy >= H) continue;
+    for (int ox = -r; ox <= r; ++ox) {
+      int xx = x + ox;
+      if (xx < 0 || xx >= W) continue;
+      size_t k = (size_t)yy * W + xx;
+      if (v[k]) {
+        double dv = d[k];
+        hi = fmax(hi, dv);
+        lo = fmin(lo, dv);
+      }
+    }
+  }
+  return (hi - lo) > gamma_e;
+}
+
+// warp one source pixel; returns true if it lands (keep test of
+// prediction.py:104-106) and fills target index and d'
+__device__ __forceinline__ bool warp_src(const double* __restrict__ Hm, const Rig& rig, int sx, int sy,
+                                         double d, uint32_t& tgt, double& dp, bool& at_inf) {
+  double xp, yp;
+  at_inf = !warp_point(Hm, (double)sx, (double)sy, d, rig.cx, rig.cy, xp, yp, dp);
+  if (at_inf) return false;
+  double tx = rint(xp), ty = rint(yp);
+  bool keep = (tx >= 0.0) && (tx < (double)rig.W) && (ty >= 0.0) && (ty < (double)rig.H) &&
+              (dp > 0.0) && (dp <= (double)rig.d_max);
+  if (!keep) return false;
+  tgt = (uint32_t)ty * (uint32_t)rig.W + (uint32_t)tx;
+  return true;
+}
+
+__global__ void k_warp_zmax(PredArgs a) {
+  const int sv = blockIdx.y;
+  const int s = sv >> 1;
+  if (!a.have_pred[s]) return;
+  const size_t HW = (size_t)a.rig.W * a.rig.H;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int)HW) return;
+  const double* d = a.sd + sv * HW;
+  const uint8_t* v = a.sv + sv * HW;
+  if (!v[i]) return;
+  const int x = i % a.rig.W, y = i / a.rig.W;
+  if (a.prm.edge_reject && is_edge(d, v, x, y, a.rig.W, a.rig.H, a.prm.edge_window, a.prm.gamma_e))
+    return;
+  uint32_t tgt;
+  double dp;
+  bool at_inf;
+  const double di = d[i];
+  if (!warp_src(a.Hm + 16 * sv, a.rig, x, y, di, tgt, dp, at_inf)) {
+    if (at_inf) atomicOr(a.err + s, ERR_POINT_AT_INFINITY);
+    return;
+  }
+  if (!(di > 0.0)) atomicOr(a.err + s, ERR_NONPOSITIVE_D);
+  atomicMax(a.zkey + sv * HW + tgt, (unsigned long long)__double_as_longlong(dp));
+}
+
+__global__ void k_warp_zidx(PredArgs a) {
+  const int sv = blockIdx.y;
+  const int s = sv >> 1;
+  if (!a.have_pred[s]) return;
+  const size_t HW = (size_t)a.rig.W * a.rig.H;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int)HW) return;
+  const double* d = a.sd + sv * HW;
+  const uint8_t* v = a.sv + sv * HW;
+  if (!v[i]) return;
+  const int x = i % a.rig.W, y = i / a.rig.W;
+  if (a.prm.edge_reject && is_edge(d, v, x, y, a.rig.W, a.rig.H, a.prm.edge_window, a.prm.gamma_e))
+    return;
+  uint32_t tgt;
+  double dp;
+  bool at_inf;
+  if (!warp_src(a.Hm + 16 * sv, a.rig, x, y, d[i], tgt, dp, at_inf)) return;
+  if ((unsigned long long)__double_as_longlong(dp) == a.zkey[sv * HW + tgt])
+    atomicMin(a.zidx + sv * HW + tgt, (uint32_t)i);
+}
+
+// predicted (d', p', valid) at target pixel t from the z-buffer winner
+// (prediction.py:67-77,123-125: p' = (d'/d)^2 p + q)
+__device__ __forceinline__ void resolve(const PredArgs& a, int sv, uint32_t t, double& od,
+                                        double& op, bool& ov) {
+  const size_t HW = (size_t)a.rig.W * a.rig.H;
+  const uint32_t src = a.zidx[sv * HW + t];
+  od = 0.0;
+  op = 0.0;
+  ov = false;
+  if (src == NO_SRC) return;
+  const double d = a.sd[sv * HW + src];
+  const double p = a.sp[sv * HW + src];
+  uint32_t tgt;
+  double dp;
+  bool at_inf;
+  warp_src(a.Hm + 16 * sv, a.rig, (int)(src % a.rig.W), (int)(src / a.rig.W), d, tgt, dp, at_inf);
+  const double ratio = dp / d;
+  od = dp;
+  op = ratio * ratio * p + a.prm.q;
+  ov = true;
+}
+
+// horizontal zoom-hole pass (prediction.py:148-166, axis=1) fused with the
+// z-buffer resolve; writes the intermediate maps
+__global__ void k_resolve_fill_h(PredArgs a) {
+  const int sv = blockIdx.y;
+  const int s = sv >> 1;
+  if (!a.have_pred[s]) return;
+  const int W = a.rig.W;
+  const size_t HW = (size_t)W * a.rig.H;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int)HW) return;
+  const int x = i % W;
+  double d, p;
+  bool v;
+  resolve(a, sv, i, d, p, v);
+  if (a.prm.fill_holes && !v && x > 0 && x < W - 1) {
+    double da, pa, db, pb;
+    bool va, vb;
+    resolve(a, sv, i - 1, da, pa, va);
+    resolve(a, sv, i + 1, db, pb, vb);
+    if (va && vb && fabs(da - db) < a.prm.gamma_f) {
+      d = 0.5 * (da + db);
+      p = fmax(pa, pb) + a.prm.q;
+      v = true;
+    }
+  }
+  a.hd[sv * HW + i] = d;
+  a.hp[sv * HW + i] = p;
+  a.hv[sv * HW + i] = v;
+}
+
+// vertical pass (axis=0) + final predicted maps + search intervals + the
+// row-ragged pair offsets.  One CTA per image row.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_fill_v_intervals(PredArgs a) {
+  __shared__ uint32_t scan_smem[32];
+  __shared__ unsigned long long cells_smem;
+  const int sv = blockIdx.y;
+  const int s = sv >> 1;
+  const int y = blockIdx.x;
+  const int W = a.rig.W, H = a.rig.H, d_max = a.rig.d_max;
+  const size_t HW = (size_t)W * H;
+  const bool pred = a.have_pred[s] != 0;
+  const int per = (W + NT - 1) / NT;
+  const int x0 = threadIdx.x * per;
+  const int x1 = min(x0 + per, W);
+  if (threadIdx.x == 0) cells_smem = 0ull;
+  // pass 1: final predicted values, intervals, this thread's pair count
+  uint32_t my_pairs = 0;
+  unsigned long long my_cells = 0;
+  for (int x = x0; x < x1; ++x) {
+    const size_t i = sv * HW + (size_t)y * W + x;
+    double d = 0.0, p = 0.0;
+    bool v = false;
+    if (pred) {
+      d = a.hd[i];
+      p = a.hp[i];
+      v = a.hv[i] != 0;
+      if (a.prm.fill_holes && !v && y > 0 && y < H - 1) {
+        const bool va = a.hv[i - W] != 0, vb = a.hv[i + W] != 0;
+        const double da = a.hd[i - W], db = a.hd[i + W];
+        if (va && vb && fabs(da - db) < a.prm.gamma_f) {
+          d = 0.5 * (da + db);
+          p = fmax(a.hp[i - W], a.hp[i + W]) + a.prm.q;
+          v = true;
+        }
+      }
+      if (!v) d = 0.0;
+    }
+    a.pd[i] = d;
+    a.pp[i] = p;
+    a.pv[i] = v;
+    int lo, hi;
+    interval_of(d, p, v, d_max, lo, hi);
+    my_pairs += (uint32_t)((hi >> 1) - (lo >> 1) + 1);
+    my_cells += (unsigned long long)(hi - lo + 1);
+    a.meta[i].x = (uint32_t)lo | ((uint32_t)hi << 16);
+  }
+  uint32_t total;
+  uint32_t base = block_exclusive_scan<NT>(my_pairs, scan_smem, total);
+  // pass 2: offsets
+  const uint32_t rowbase = (uint32_t)y * (uint32_t)(W * npairs_max(d_max));
+  for (int x = x0; x < x1; ++x) {
+    const size_t i = sv * HW + (size_t)y * W + x;
+    const uint32_t m = a.meta[i].x;
+    a.meta[i].y = rowbase + base;
+    base += ((m >> 16) >> 1) - ((m & 0xFFFFu) >> 1) + 1;
+  }
+  atomicAdd(&cells_smem, my_cells);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(a.cells + sv, cells_smem);
+}
+
+// meta from caller-supplied intervals (stage-level matching_cost / variance)
+template <int NT>
+__global__ void __launch_bounds__(NT) k_meta_from_intervals(const int64_t* __restrict__ lo_in,
+                                                            const int64_t* __restrict__ hi_in,
+                                                            int W, int H, int d_max,
+                                                            uint2* __restrict__ meta) {
+  __shared__ uint32_t scan_smem[32];
+  const int y = blockIdx.x;
+  const int per = (W + NT - 1) / NT;
+  const int x0 = threadIdx.x * per;
+  const int x1 = min(x0 + per, W);
+  uint32_t my_pairs = 0;
+  for (int x = x0; x < x1; ++x) {
+    const size_t i = (size_t)y * W + x;
+    const uint32_t lo = (uint32_t)lo_in[i], hi = (uint32_t)hi_in[i];
+    my_pairs += (hi >> 1) - (lo >> 1) + 1;
+    meta[i].x = lo | (hi << 16);
+  }
+  uint32_t total;
+  uint32_t base = block_exclusive_scan<NT>(my_pairs, scan_smem, total);
+  const uint32_t rowbase = (uint32_t)y * (uint32_t)(W * npairs_max(d_max));
+  for (int x = x0; x < x1; ++x) {
+    const size_t i = (size_t)y * W + x;
+    const uint32_t m = meta[i].x;
+    meta[i].y = rowbase + base;
+    base += ((m >> 16) >> 1) - ((m & 0xFFFFu) >> 1) + 1;
+  }
+}
+
+// stage-level edge mask (reject_edges)
+__global__ void k_edges(const double* __restrict__ d, const uint8_t* __restrict__ v, int W, int H,
+                        int r, double gamma_e, uint8_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= W * H) return;
+  out[i] = v[i] && is_edge(d, v, i % W, i / W, W, H, r, gamma_e);
+}
+
+// ---------------------------------------------------------------- launchers
+
+void launch_predict(const PredArgs& a, int n_sv, cudaStream_t st) {
+  const int HW = a.rig.W * a.rig.H;
+  dim3 grid((HW + 255) / 256, n_sv);
+  cudaMemsetAsync(a.zkey, 0, sizeof(unsigned long long) * (size_t)HW * n_sv, st);
+  cudaMemsetAsync(a.zidx, 0xFF, sizeof(uint32_t) * (size_t)HW * n_sv, st);
+  k_warp_zmax<<<grid, 256, 0, st>>>(a);
+  k_warp_zidx<<<grid, 256, 0, st>>>(a);
+  k_resolve_fill_h<<<grid, 256, 0, st>>>(a);
+}
+
+void launch_fill_v_intervals(const PredArgs& a, int n_sv, cudaStream_t st) {
+  cudaMemsetAsync(a.cells, 0, sizeof(unsigned long long) * n_sv, st);
+  k_fill_v_intervals<256><<<dim3(a.rig.H, n_sv), 256, 0, st>>>(a);
+}
+
+void launch_meta_from_intervals(const int64_t* lo, const int64_t* hi, int W, int H, int d_max,
+                                uint2* meta, cudaStream_t st) {
+  k_meta_from_intervals<256><<<H, 256, 0, st>>>(lo, hi, W, H, d_max, meta);
+}
+
+void launch_edges(const double* d, const uint8_t* v, int W, int H, int r, double gamma_e,
+                  uint8_t* out, cudaStream_t st) {
+  k_edges<<<(W * H + 255) / 256, 256, 0, st>>>(d, v, W, H, r, gamma_e, out);
+}
+
+}  // namespace es

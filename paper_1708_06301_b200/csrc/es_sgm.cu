@@ -1,0 +1,450 @@
+// K4 + K5: 8-path SGM aggregation over the ragged cost volume, then
+// winner-take-all and the matching-variance walk.
+//
+// Reference: sgm.py:199-272 (_path_step, _scan_vertical, _scan_horizontal,
+// aggregate_paths), sgm.py:275-344 (select_disparity, matching_variance_map).
+//
+// Paths are independent chains of pixels: rows (H), columns (V), x-y = const
+// (D1) and x+y = const (D2).  One warp owns one chain and walks it; lane l
+// holds pair c*32 + l of chunk c (pair j = cells 2j, 2j+1) so a pixel's
+// interval touches only chunks (lo>>1)/32 .. (hi>>1)/32, a warp-uniform
+// range: reduced intervals cost one chunk per step, full range
+// ceil((d_max+1)/64).  The predecessor's values stay in registers; d-1 / d+1
+// neighbours come from one rotated shuffle each plus a byte permute.
+//
+// Arithmetic policies:
+//   U16 (default integer penalties, small windows): two cells per 32-bit word,
+//     VIMNMX.U16x2 / VIADDMNMX.U16x2 / VIADD.16x2.  "+inf" is 0x8000; sums
+//     are exact because every finite value is <= window^2*255 + P2 and the
+//     8-path sum stays < 2^16 (host-checked), while out-of-interval values
+//     stay in [0x8000, 0x8000 + P2] and are never selected.
+//   F32 (any other penalties / volumes): float2 per lane, numpy's float32
+//     operation order, 8 single-direction launches in the reference's
+//     summation order (H->, H<-, dy=+1 dx=-1,0,1, dy=-1 dx=-1,0,1).
+#include "es_common.cuh"
+#include "es_kernels.h"
+
+namespace es {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int SGM_WARPS = 4;
+
+// ------------------------------------------------------------ policies
+
+struct U16A {
+  using P = uint32_t;
+  __device__ static __forceinline__ P inf() { return INF16x2; }
+  __device__ static __forceinline__ P load_cost(const void* C, size_t k) {
+    return __ldg(reinterpret_cast<const uint32_t*>(C) + k);
+  }
+  __device__ static __forceinline__ P step(P cv, P pv, P pl, P pr, const SgmArgs& a, P mP2,
+                                           P negm) {
+    const P left = __byte_perm(pl, pv, 0x5432);
+    const P right = __byte_perm(pv, pr, 0x5432);
+    const P nb = __vminu2(left, right);
+    const P p1 = a.p1i | (a.p1i << 16);
+    const P cand = __vminu2(__viaddmin_u16x2(nb, p1, pv), mP2);
+    return __vadd2(cv, __vadd2(cand, negm));
+  }
+  __device__ static __forceinline__ P vmin(P a, P b) { return __vminu2(a, b); }
+  __device__ static __forceinline__ uint32_t warp_min(P v) {
+    return __reduce_min_sync(FULL, min(v & 0xFFFFu, v >> 16));
+  }
+  __device__ static __forceinline__ P splat_m_p2(uint32_t m, const SgmArgs& a) {
+    const uint32_t s = m + a.p2i;
+    return s | (s << 16);
+  }
+  __device__ static __forceinline__ P negm(uint32_t m) {
+    const uint32_t n = (0x10000u - m) & 0xFFFFu;
+    return n | (n << 16);
+  }
+  __device__ static __forceinline__ void store_sum(void* S, size_t k, P L, bool init) {
+    uint32_t* s = reinterpret_cast<uint32_t*>(S) + k;
+    *s = init ? L : __vadd2(*s, L);
+  }
+};
+
+struct F32A {
+  using P = float2;
+  __device__ static __forceinline__ P inf() { return make_float2(INFINITY, INFINITY); }
+  __device__ static __forceinline__ P load_cost_u16(const void* C, size_t k) {
+    const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(C) + k);
+    const uint32_t a = w & 0xFFFFu, b = w >> 16;
+    return make_float2(a >= INF16 ? INFINITY : (float)a, b >= INF16 ? INFINITY : (float)b);
+  }
+  __device__ static __forceinline__ P step(P cv, P pv, P pl, P pr, const SgmArgs& a, P mP2,
+                                           P m) {
+    // numpy order (sgm.py:205-209): cand = min(prev, m+p2), then the two
+    // neighbour terms prev[d-1]+p1, prev[d+1]+p1; out = cost + (cand - m)
+    const float l0 = pl.y, l1 = pv.x;   // prev[d-1] for the two cells
+    const float r0 = pv.y, r1 = pr.x;   // prev[d+1]
+    float c0 = fminf(pv.x, mP2.x), c1 = fminf(pv.y, mP2.y);
+    c0 = fminf(c0, __fadd_rn(l0, a.p1));
+    c1 = fminf(c1, __fadd_rn(l1, a.p1));
+    c0 = fminf(c0, __fadd_rn(r0, a.p1));
+    c1 = fminf(c1, __fadd_rn(r1, a.p1));
+    return make_float2(__fadd_rn(cv.x, __fsub_rn(c0, m.x)), __fadd_rn(cv.y, __fsub_rn(c1, m.y)));
+  }
+  __device__ static __forceinline__ P vmin(P a, P b) {
+    return make_float2(fminf(a.x, b.x), fminf(a.y, b.y));
+  }
+  __device__ static __forceinline__ float warp_min(P v) {
+    float x = fminf(v.x, v.y);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x = fminf(x, __shfl_xor_sync(FULL, x, o));
+    return x;
+  }
+  __device__ static __forceinline__ P splat_m_p2(float m, const SgmArgs& a) {
+    const float s = __fadd_rn(m, a.p2);
+    return make_float2(s, s);
+  }
+  __device__ static __forceinline__ P negm(float m) { return make_float2(m, m); }
+  __device__ static __forceinline__ void store_sum(void* S, size_t k, P L, bool init) {
+    float2* s = reinterpret_cast<float2*>(S) + k;
+    if (init) {
+      *s = L;
+    } else {
+      float2 o = *s;
+      *s = make_float2(__fadd_rn(o.x, L.x), __fadd_rn(o.y, L.y));
+    }
+  }
+};
+
+__device__ __forceinline__ uint32_t shfl_u(uint32_t v, int src) { return __shfl_sync(FULL, v, src); }
+__device__ __forceinline__ float2 shfl_u(float2 v, int src) {
+  return make_float2(__shfl_sync(FULL, v.x, src), __shfl_sync(FULL, v.y, src));
+}
+
+// chain geometry: start pixel, step, length for (family, sweep, chain)
+__device__ __forceinline__ void chain_geom(int fam, int bwd, int c, int W, int H, int& x0, int& y0,
+                                           int& sx, int& sy, int& len) {
+  if (fam == FAM_H) {
+    sy = 0;
+    y0 = c;
+    len = W;
+    sx = bwd ? -1 : 1;
+    x0 = bwd ? W - 1 : 0;
+  } else if (fam == FAM_V) {
+    sx = 0;
+    x0 = c;
+    len = H;
+    sy = bwd ? -1 : 1;
+    y0 = bwd ? H - 1 : 0;
+  } else {
+    int ya, yb;   // y range of the diagonal
+    if (fam == FAM_D1) {   // x - y = u
+      const int u = c - (H - 1);
+      ya = max(0, -u);
+      yb = min(H - 1, W - 1 - u);
+      len = yb - ya + 1;
+      y0 = bwd ? yb : ya;
+      x0 = u + y0;
+      sy = bwd ? -1 : 1;
+      sx = sy;
+    } else {               // x + y = s
+      const int s = c;
+      ya = max(0, s - (W - 1));
+      yb = min(H - 1, s);
+      len = yb - ya + 1;
+      y0 = bwd ? yb : ya;
+      x0 = s - y0;
+      sy = bwd ? -1 : 1;
+      sx = -sy;
+    }
+  }
+}
+
+template <class A, int NCH, bool COST_F32>
+__global__ void __launch_bounds__(SGM_WARPS * 32) k_sgm(SgmArgs a, int fam, int sweeps, int init) {
+  using P = typename A::P;
+  const int lane = threadIdx.x & 31;
+  const int chain = blockIdx.x * SGM_WARPS + (threadIdx.x >> 5);
+  const int W = a.W, H = a.H;
+  const int nchains = fam == FAM_H ? H : (fam == FAM_V ? W : W + H - 1);
+  if (chain >= nchains) return;
+  const size_t HW = (size_t)W * H;
+  const uint2* meta = a.meta + (size_t)blockIdx.y * HW;
+  const size_t vbase = (size_t)blockIdx.y * a.volcap;
+  bool first_sweep = true;
+  for (int bwd = 0; bwd < 2; ++bwd) {
+    if (!(sweeps & (1 << bwd))) continue;
+    const bool init_sum = init && first_sweep;
+    first_sweep = false;
+    int x, y, sx, sy, len;
+    chain_geom(fam, bwd, chain, W, H, x, y, sx, sy, len);
+    P prev[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) prev[c] = A::inf();
+    decltype(A::warp_min(A::inf())) m = 0;
+    for (int t = 0; t < len; ++t, x += sx, y += sy) {
+      const uint2 mt = meta[(size_t)y * W + x];
+      const int j0 = (int)(lo_of(mt) >> 1), j1 = (int)(hi_of(mt) >> 1);
+      const int clo = j0 >> 5, chi = j1 >> 5;
+      const P mP2 = A::splat_m_p2(m, a);
+      const P ng = A::negm(m);
+      P cur[NCH];
+      P nmin = A::inf();
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        if (c < clo || c > chi) {
+          cur[c] = A::inf();
+          continue;
+        }
+        const int j = c * 32 + lane;
+        const bool in = j >= j0 && j <= j1;
+        const size_t k = vbase + mt.y + (size_t)(j - j0);
+        P cv = A::inf();
+        if (in) {
+          if constexpr (COST_F32) {
+            cv = __ldg(reinterpret_cast<const float2*>(a.C) + k);
+          } else if constexpr (sizeof(P) == 4) {
+            cv = A::load_cost(a.C, k);
+          } else {
+            cv = F32A::load_cost_u16(a.C, k);
+          }
+        }
+        P L;
+        if (t == 0) {
+          L = cv;
+        } else {
+          const P srcl = lane == 31 ? (c > 0 ? prev[c > 0 ? c - 1 : 0] : A::inf()) : prev[c];
+          const P pl = shfl_u(srcl, (lane + 31) & 31);
+          const P srcr = lane == 0 ? (c + 1 < NCH ? prev[c + 1 < NCH ? c + 1 : c] : A::inf()) : prev[c];
+          const P pr = shfl_u(srcr, (lane + 1) & 31);
+          L = A::step(cv, prev[c], pl, pr, a, mP2, ng);
+        }
+        cur[c] = L;
+        nmin = A::vmin(nmin, L);
+        if (in) A::store_sum(a.S, k, L, init_sum);
+      }
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) prev[c] = cur[c];
+      m = A::warp_min(nmin);
+    }
+  }
+}
+
+template <class A, bool CF32>
+static void launch_family(const SgmArgs& a, int nch, int fam, int sweeps, int init, int n_sv,
+                          cudaStream_t st) {
+  const int nchains = fam == FAM_H ? a.H : (fam == FAM_V ? a.W : a.W + a.H - 1);
+  dim3 grid((nchains + SGM_WARPS - 1) / SGM_WARPS, n_sv);
+  const int bs = SGM_WARPS * 32;
+  switch (nch) {
+    case 1: k_sgm<A, 1, CF32><<<grid, bs, 0, st>>>(a, fam, sweeps, init); break;
+    case 2: k_sgm<A, 2, CF32><<<grid, bs, 0, st>>>(a, fam, sweeps, init); break;
+    case 3: k_sgm<A, 3, CF32><<<grid, bs, 0, st>>>(a, fam, sweeps, init); break;
+    case 4: k_sgm<A, 4, CF32><<<grid, bs, 0, st>>>(a, fam, sweeps, init); break;
+    default: k_sgm<A, 8, CF32><<<grid, bs, 0, st>>>(a, fam, sweeps, init); break;
+  }
+}
+
+void launch_aggregate(const SgmArgs& a, int arith, int n_sv, cudaStream_t st) {
+  int nch = (npairs_max(a.d_max) + 31) / 32;
+  if (nch > 4) nch = 8;
+  if (arith == ARITH_U16) {
+    launch_family<U16A, false>(a, nch, FAM_H, 3, 1, n_sv, st);
+    launch_family<U16A, false>(a, nch, FAM_V, 3, 0, n_sv, st);
+    launch_family<U16A, false>(a, nch, FAM_D1, 3, 0, n_sv, st);
+    launch_family<U16A, false>(a, nch, FAM_D2, 3, 0, n_sv, st);
+  } else {
+    // reference order: H->, H<-, (-1,+1), (0,+1), (+1,+1), (-1,-1), (0,-1), (+1,-1)
+    static const int order[8][2] = {{FAM_H, 1}, {FAM_H, 2}, {FAM_D2, 1}, {FAM_V, 1},
+                                    {FAM_D1, 1}, {FAM_D1, 2}, {FAM_V, 2}, {FAM_D2, 2}};
+    for (int k = 0; k < 8; ++k) {
+      if (a.cost_f32)
+        launch_family<F32A, true>(a, nch, order[k][0], order[k][1], k == 0, n_sv, st);
+      else
+        launch_family<F32A, false>(a, nch, order[k][0], order[k][1], k == 0, n_sv, st);
+    }
+  }
+}
+
+// ------------------------------------------------------------ WTA + variance
+
+// One warp per pixel: argmin over the interval (ties -> smaller d,
+// sgm.py:282), then the outward walk of sgm.py:319-344 by lane 0.
+template <bool F32>
+__global__ void __launch_bounds__(256) k_wta_var(WtaArgs a) {
+  const int lane = threadIdx.x & 31;
+  const size_t HW = (size_t)a.W * a.H;
+  const size_t pix = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (pix >= HW) return;
+  const int svl = blockIdx.y;
+  const uint2 mt = a.meta[svl * HW + pix];
+  const int lo = lo_of(mt), hi = hi_of(mt);
+  const int j0 = lo >> 1, j1 = hi >> 1;
+  const size_t base = svl * a.volcap + mt.y;
+  float bestv = INFINITY;
+  int bestd = 0x7fffffff;
+  if (a.dstar_in == nullptr) {
+    for (int j = j0 + lane; j <= j1; j += 32) {
+      float v0, v1;
+      if constexpr (F32) {
+        const float2 w = reinterpret_cast<const float2*>(a.S)[base + (j - j0)];
+        v0 = w.x;
+        v1 = w.y;
+      } else {
+        const uint32_t w = reinterpret_cast<const uint32_t*>(a.S)[base + (j - j0)];
+        v0 = (float)(w & 0xFFFFu);
+        v1 = (float)(w >> 16);
+      }
+      const int d0 = 2 * j, d1 = 2 * j + 1;
+      if (d0 >= lo && d0 <= hi && (v0 < bestv || (v0 == bestv && d0 < bestd))) { bestv = v0; bestd = d0; }
+      if (d1 >= lo && d1 <= hi && (v1 < bestv || (v1 == bestv && d1 < bestd))) { bestv = v1; bestd = d1; }
+    }
+  #pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float ov = __shfl_xor_sync(FULL, bestv, o);
+      const int od = __shfl_xor_sync(FULL, bestd, o);
+      if (ov < bestv || (ov == bestv && od < bestd)) { bestv = ov; bestd = od; }
+    }
+    if (bestd == 0x7fffffff) bestd = 0;   // all +inf: numpy argmin -> index 0
+  }
+  if (lane != 0) return;
+  auto cell = [&](int d) -> float {
+    const int jj = (d >> 1) - j0;
+    if constexpr (F32) {
+      const float2 w = reinterpret_cast<const float2*>(a.S)[base + jj];
+      return (d & 1) ? w.y : w.x;
+    } else {
+      const uint32_t w = reinterpret_cast<const uint32_t*>(a.S)[base + jj];
+      return (float)((d & 1) ? (w >> 16) : (w & 0xFFFFu));
+    }
+  };
+  if (a.dstar_in) {
+    bestd = a.dstar_in[svl * HW + pix];
+    bestv = (bestd >= lo && bestd <= hi) ? cell(bestd) : INFINITY;
+  }
+  const float cstar = bestv;
+  long long count = 0;
+  double s = 0.0;
+  const bool inside = bestd >= lo && bestd <= hi;   // false only for all-inf pixels
+  for (int d = bestd - 1; inside && d >= lo; --d) {
+    s += (double)__fsub_rn(cell(d), cstar);
+    if (!(s < a.s_max)) break;
+    ++count;
+  }
+  s = 0.0;
+  for (int d = bestd + 1; inside && d <= hi; ++d) {
+    s += (double)__fsub_rn(cell(d), cstar);
+    if (!(s < a.s_max)) break;
+    ++count;
+  }
+  const size_t o = svl * HW + pix;
+  a.dstar[o] = (uint16_t)bestd;
+  a.valid[o] = bestd > 0;
+  a.r[o] = fmax((double)count, a.r_min);
+}
+
+void launch_wta_variance(const WtaArgs& a, int n_sv, cudaStream_t st) {
+  const size_t HW = (size_t)a.W * a.H;
+  dim3 grid((unsigned)((HW + 7) / 8), n_sv);
+  if (a.arith == ARITH_U16) k_wta_var<false><<<grid, 256, 0, st>>>(a);
+  else k_wta_var<true><<<grid, 256, 0, st>>>(a);
+}
+
+// ------------------------------------------------------------ converters
+
+__global__ void k_export_dense(const uint2* __restrict__ meta, const void* __restrict__ vol,
+                               int vol_f32, int W, int H, int D, float* __restrict__ out) {
+  const size_t HW = (size_t)W * H;
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= HW * D) return;
+  const size_t pix = idx / D;
+  const int d = (int)(idx % D);
+  const uint2 mt = meta[pix];
+  const int lo = lo_of(mt), hi = hi_of(mt);
+  float v = INFINITY;
+  if (d >= lo && d <= hi) {
+    const size_t k = (size_t)mt.y + (size_t)((d >> 1) - (lo >> 1));
+    if (vol_f32 == EXPORT_F32) {
+      const float2 w = reinterpret_cast<const float2*>(vol)[k];
+      v = (d & 1) ? w.y : w.x;
+    } else {
+      const uint32_t w = reinterpret_cast<const uint32_t*>(vol)[k];
+      const uint32_t h = (d & 1) ? (w >> 16) : (w & 0xFFFFu);
+      // u16 costs use 0x8000 as +inf; u16 sums are always finite in-interval
+      v = (vol_f32 == EXPORT_U16_COST && h >= INF16) ? INFINITY : (float)h;
+    }
+  }
+  out[idx] = v;
+}
+
+void launch_export_dense(const uint2* meta, const void* vol, int vol_f32, int W, int H, int d_max,
+                         float* out, cudaStream_t st) {
+  const size_t n = (size_t)W * H * (d_max + 1);
+  k_export_dense<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(meta, vol, vol_f32, W, H, d_max + 1,
+                                                               out);
+}
+
+// dense (H, W, D) float32 -> ragged pairs (u16 when as_f32 == 0)
+__global__ void k_import_dense(const float* __restrict__ dense, const uint2* __restrict__ meta,
+                               int W, int H, int D, int as_f32, void* __restrict__ vol) {
+  const size_t pix = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= (size_t)W * H) return;
+  const uint2 mt = meta[pix];
+  const int lo = lo_of(mt), hi = hi_of(mt);
+  for (int j = lo >> 1; j <= (hi >> 1); ++j) {
+    const size_t k = (size_t)mt.y + (size_t)(j - (lo >> 1));
+    float v[2];
+    for (int h = 0; h < 2; ++h) {
+      const int d = 2 * j + h;
+      v[h] = (d >= lo && d <= hi) ? dense[pix * D + d] : INFINITY;
+    }
+    if (as_f32) {
+      reinterpret_cast<float2*>(vol)[k] = make_float2(v[0], v[1]);
+    } else {
+      uint32_t w = 0;
+      for (int h = 0; h < 2; ++h) w |= (isinf(v[h]) ? INF16 : (uint32_t)v[h]) << (16 * h);
+      reinterpret_cast<uint32_t*>(vol)[k] = w;
+    }
+  }
+}
+
+void launch_import_dense(const float* dense, const uint2* meta, int W, int H, int D, int as_f32,
+                         void* vol, cudaStream_t st) {
+  const size_t HW = (size_t)W * H;
+  k_import_dense<<<(unsigned)((HW + 127) / 128), 128, 0, st>>>(dense, meta, W, H, D, as_f32, vol);
+}
+
+// per-pixel hull [first finite d, last finite d] of a dense volume, plus
+// flags: bit0 = some finite value is negative, non-integral or >= limit;
+// bit1 = some pixel has no finite value; bit2 = NaN present; bit3 = +inf
+// strictly inside a pixel's hull
+__global__ void k_hull(const float* __restrict__ dense, int W, int H, int D, int64_t* lo,
+                       int64_t* hi, unsigned int* flags, float limit) {
+  const size_t pix = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= (size_t)W * H) return;
+  int first = -1, last = -1, nfin = 0;
+  unsigned f = 0;
+  for (int d = 0; d < D; ++d) {
+    const float v = dense[pix * D + d];
+    if (isnan(v)) f |= 4u;
+    if (isfinite(v)) {
+      if (first < 0) first = d;
+      last = d;
+      ++nfin;
+      if (v < 0.0f || v != floorf(v) || v >= limit) f |= 1u;
+    }
+  }
+  if (first < 0) {
+    f |= 2u;
+    first = 0;
+    last = 0;
+  }
+  else if (nfin != last - first + 1) {
+    f |= 8u;   // +inf inside the hull: the u16 path cannot represent it
+  }
+  lo[pix] = first;
+  hi[pix] = last;
+  if (f) atomicOr(flags, f);
+}
+
+void launch_hull(const float* dense, int W, int H, int D, int64_t* lo, int64_t* hi,
+                 unsigned int* flags, float limit, cudaStream_t st) {
+  const size_t HW = (size_t)W * H;
+  k_hull<<<(unsigned)((HW + 127) / 128), 128, 0, st>>>(dense, W, H, D, lo, hi, flags, limit);
+}
+
+}  // namespace es

@@ -1,0 +1,354 @@
+"""Per-frame engine: drop-in for ``egostereo.pipeline`` (pipeline.py:53-302).
+
+``DisparityPipeline.process_frame`` (pipeline.py:108-170) runs the whole
+frame on the B200 through one ``es_ctx_step`` call: warp + z-buffer + Kalman
+predict, hole fill, intervals, ragged SAD cost, 8-path SGM, WTA + variance,
+LR + SAD checks and the Kalman update.  The filter state stays resident in
+HBM (double-buffered); ``FrameResult`` maps are copied to the host only when
+read (``FrameResult`` materialises itself before the engine overwrites the
+buffers it refers to).
+
+``BatchedPipeline`` advances B independent sequences per call (config 5,
+SURVEY 8(e)); multi-GPU runs shard sequences across processes.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .core import (DisparityMap, FilterState, StereoRig, VarianceMap, make_empty_state,
+                   validate_rigid_motion)
+from .fusion import FusionParams
+from .geometry import disparity_homography, right_motion
+from .prediction import PredictionParams
+from .sgm import IntervalMap, SgmParams
+
+__all__ = ["FrameResult", "PipelineParams", "DisparityPipeline", "BatchedPipeline",
+           "Sequence", "relative_motions", "run_sequence", "StereoEngine"]
+
+
+@dataclass
+class PipelineParams:
+    """pipeline.py:75-82."""
+
+    sgm: SgmParams = field(default_factory=SgmParams)
+    prediction: PredictionParams = field(default_factory=PredictionParams)
+    fusion: FusionParams = field(default_factory=FusionParams)
+    baseline: bool = False
+
+
+_U8_MAPS = {_lib.ES_PRED_VALID, _lib.ES_MEAS_VALID, _lib.ES_KEEP, _lib.ES_FUSED_VALID}
+_I64_MAPS = {_lib.ES_LO, _lib.ES_HI}
+
+
+class StereoEngine:
+    """Owner of one ``es_ctx``: B sequences of one rig on one device."""
+
+    def __init__(self, rig, params: PipelineParams | None = None, batch: int = 1,
+                 device: int = 0):
+        self.rig = rig
+        self.params = params or PipelineParams()
+        self.batch = int(batch)
+        self.device = int(device)
+        self._rs = _lib.rig_struct(rig)
+        p = self.params
+        self._ps = _lib.params_struct(p.sgm, p.prediction, p.fusion, p.baseline)
+        h = ctypes.c_void_p()
+        _lib.call("es_ctx_create", self.device, ctypes.byref(self._rs), ctypes.byref(self._ps),
+                  self.batch, ctypes.byref(h))
+        self._h = h
+        self.generation = 0
+        self._Hm = np.zeros((self.batch, 2, 16), np.float64)
+        self._given = np.zeros(self.batch, np.uint8)
+        self._have_state = np.zeros(self.batch, bool)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            _lib.load().es_ctx_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reset(self):
+        _lib.call("es_ctx_reset", self._h)
+        self._have_state[:] = False
+        self.generation += 1
+
+    def homographies(self, motions):
+        """Host-side 4x4 builds (geometry.py:62-92) for sequences that will
+        predict; the device receives 16 doubles per view."""
+        self._given[:] = 0
+        for s, T in enumerate(motions):
+            if T is None or self.params.baseline or not self._have_state[s]:
+                continue
+            T = validate_rigid_motion(T)
+            self._Hm[s, 0] = disparity_homography(self.rig, T).ravel()
+            self._Hm[s, 1] = disparity_homography(self.rig, right_motion(self.rig, T)).ravel()
+            self._given[s] = 1
+
+    def step(self, images, motions, sync: bool = True, images_dev: int | None = None):
+        """Advance every sequence one frame.  ``images`` is a host uint8
+        array (B, 2, H, W) or, with ``images_dev``, a device pointer."""
+        self.homographies(motions)
+        if images_dev is None:
+            img = _lib.c_array(images, np.uint8)
+            if img.shape != (self.batch, 2, self.rig.height, self.rig.width):
+                raise ValueError(f"images must be (B, 2, H, W), got {img.shape}")
+            src, on_dev = _lib.ptr(img), 0
+        else:
+            src, on_dev = ctypes.c_void_p(images_dev), 1
+        self.generation += 1
+        _lib.call("es_ctx_step", self._h, src, on_dev, _lib.ptr(self._Hm), _lib.ptr(self._given),
+                  1 if sync else 0)
+        if sync:
+            self._refresh_state_flags()
+        else:
+            self._have_state[:] = True
+
+    def sync(self):
+        _lib.call("es_ctx_sync", self._h)
+        self._refresh_state_flags()
+
+    def _refresh_state_flags(self):
+        # have_state (pipeline.py:122): any valid pixel in either view, as
+        # counted on the device by the Kalman-update step
+        f = ctypes.c_int64()
+        for s in range(self.batch):
+            _lib.call("es_ctx_have_state", self._h, s, ctypes.byref(f))
+            self._have_state[s] = bool(f.value)
+
+    def export(self, what: int, seq: int = 0, view: int = 0) -> np.ndarray:
+        h, w = self.rig.height, self.rig.width
+        if what in (_lib.ES_COST_DENSE, _lib.ES_TOTAL_DENSE):
+            out = np.empty((h, w, self.rig.d_max + 1), np.float32)
+        elif what == _lib.ES_FUSED_KITTI:
+            out = np.empty((h, w), np.uint16)
+        elif what in _U8_MAPS:
+            out = np.empty((h, w), np.uint8)
+        elif what in _I64_MAPS:
+            out = np.empty((h, w), np.int64)
+        else:
+            out = np.empty((h, w), np.float64)
+        _lib.call("es_ctx_export", self._h, int(what), int(seq), int(view), _lib.ptr(out))
+        return out.astype(bool) if what in _U8_MAPS else out
+
+    def cells(self, seq: int = 0):
+        l, r = ctypes.c_uint64(), ctypes.c_uint64()
+        _lib.call("es_ctx_cells", self._h, int(seq), ctypes.byref(l), ctypes.byref(r))
+        return int(l.value), int(r.value)
+
+    def frame(self, seq: int = 0) -> int:
+        f = ctypes.c_int64()
+        _lib.call("es_ctx_frame", self._h, int(seq), ctypes.byref(f))
+        return int(f.value)
+
+    def stream(self) -> int:
+        s = ctypes.c_void_p()
+        _lib.call("es_ctx_stream", self._h, ctypes.byref(s))
+        return s.value or 0
+
+
+class FrameResult:
+    """Everything the pipeline derived for one frame (pipeline.py:53-72).
+
+    Maps are read from the device on first access; the owning pipeline
+    forces materialisation before its next step overwrites them."""
+
+    _FIELDS = ("predicted_left", "predicted_left_var", "predicted_right", "predicted_right_var",
+               "intervals_left", "intervals_right", "measured_left", "measured_left_var",
+               "measured_right", "measured_right_var", "keep_left", "keep_right", "fused")
+
+    def __init__(self, engine: StereoEngine, seq: int, frame: int):
+        self._engine = engine
+        self._seq = seq
+        self._gen = engine.generation
+        self._cache = {}
+        self.frame = frame
+        l, r = engine.cells(seq)
+        total = engine.rig.width * engine.rig.height * (engine.rig.d_max + 1)
+        self.search_fraction_left = float(l / total)
+        self.search_fraction_right = float(r / total)
+
+    def _get(self, what, view):
+        key = (what, view)
+        if key not in self._cache:
+            if self._engine.generation != self._gen:
+                raise RuntimeError("FrameResult maps were overwritten by a later frame")
+            self._cache[key] = self._engine.export(what, self._seq, view)
+        return self._cache[key]
+
+    def materialize(self):
+        for name in self._FIELDS:
+            getattr(self, name)
+        return self
+
+    def _pred(self, v):
+        return DisparityMap(self._get(_lib.ES_PRED_D, v), self._get(_lib.ES_PRED_VALID, v))
+
+    def _meas(self, v):
+        return DisparityMap(self._get(_lib.ES_MEAS_D, v), self._get(_lib.ES_MEAS_VALID, v))
+
+    def _iv(self, v):
+        return IntervalMap(self._get(_lib.ES_LO, v), self._get(_lib.ES_HI, v),
+                           self._engine.rig.d_max)
+
+    predicted_left = property(lambda s: s._pred(0))
+    predicted_right = property(lambda s: s._pred(1))
+    predicted_left_var = property(lambda s: VarianceMap(s._get(_lib.ES_PRED_P, 0)))
+    predicted_right_var = property(lambda s: VarianceMap(s._get(_lib.ES_PRED_P, 1)))
+    intervals_left = property(lambda s: s._iv(0))
+    intervals_right = property(lambda s: s._iv(1))
+    measured_left = property(lambda s: s._meas(0))
+    measured_right = property(lambda s: s._meas(1))
+    measured_left_var = property(lambda s: VarianceMap(s._get(_lib.ES_MEAS_R, 0)))
+    measured_right_var = property(lambda s: VarianceMap(s._get(_lib.ES_MEAS_R, 1)))
+    keep_left = property(lambda s: s._get(_lib.ES_KEEP, 0))
+    keep_right = property(lambda s: s._get(_lib.ES_KEEP, 1))
+
+    @property
+    def fused(self) -> FilterState:
+        return FilterState(
+            DisparityMap(self._get(_lib.ES_FUSED_D, 0), self._get(_lib.ES_FUSED_VALID, 0)),
+            VarianceMap(self._get(_lib.ES_FUSED_P, 0)),
+            DisparityMap(self._get(_lib.ES_FUSED_D, 1), self._get(_lib.ES_FUSED_VALID, 1)),
+            VarianceMap(self._get(_lib.ES_FUSED_P, 1)),
+            frame=self.frame)
+
+    def cost_volume(self, view: int = 0) -> np.ndarray:
+        """Dense export of the raw cost (parity / debugging)."""
+        return self._get(_lib.ES_COST_DENSE, view)
+
+    def total_volume(self, view: int = 0) -> np.ndarray:
+        """Dense export of the aggregated cost (parity / debugging)."""
+        return self._get(_lib.ES_TOTAL_DENSE, view)
+
+
+class DisparityPipeline:
+    """Stateful per-sequence engine (pipeline.py:90-170) on one B200."""
+
+    def __init__(self, rig: StereoRig, params: PipelineParams | None = None, device: int = 0):
+        self.rig = rig
+        self.params = params or PipelineParams()
+        self._engine = StereoEngine(rig, self.params, batch=1, device=device)
+        self._last = None
+        self._img = np.empty((1, 2, rig.height, rig.width), np.uint8)
+
+    def reset(self) -> None:
+        self._flush()
+        self._engine.reset()
+
+    @property
+    def state(self) -> FilterState:
+        f = self._engine.frame(0)
+        if f < 0:
+            return make_empty_state(self.rig, frame=-1)
+        e = self._engine
+        return FilterState(
+            DisparityMap(e.export(_lib.ES_FUSED_D, 0, 0), e.export(_lib.ES_FUSED_VALID, 0, 0)),
+            VarianceMap(e.export(_lib.ES_FUSED_P, 0, 0)),
+            DisparityMap(e.export(_lib.ES_FUSED_D, 0, 1), e.export(_lib.ES_FUSED_VALID, 0, 1)),
+            VarianceMap(e.export(_lib.ES_FUSED_P, 0, 1)), frame=f)
+
+    def _flush(self):
+        last = self._last() if self._last is not None else None
+        if last is not None:
+            last.materialize()
+        self._last = None
+
+    def process_frame(self, left, right, motion=None) -> FrameResult:
+        """Advance the filter by one stereo pair (pipeline.py:108-170)."""
+        L = left.data if hasattr(left, "data") else np.asarray(left)
+        R = right.data if hasattr(right, "data") else np.asarray(right)
+        if L.shape != self.rig.shape or R.shape != self.rig.shape:
+            raise ValueError(f"image dimensions {L.shape}/{R.shape} != rig {self.rig.shape}")
+        self._flush()
+        self._img[0, 0] = L
+        self._img[0, 1] = R
+        self._engine.step(self._img, [motion], sync=True)
+        res = FrameResult(self._engine, 0, self._engine.frame(0))
+        self._last = weakref.ref(res)
+        return res
+
+
+class BatchedPipeline:
+    """B independent sequences advanced together (config 5)."""
+
+    def __init__(self, rig: StereoRig, batch: int, params: PipelineParams | None = None,
+                 device: int = 0):
+        self.rig = rig
+        self.batch = batch
+        self.params = params or PipelineParams()
+        self.engine = StereoEngine(rig, self.params, batch=batch, device=device)
+
+    def reset(self):
+        self.engine.reset()
+
+    def process_frames(self, images, motions, sync: bool = True, images_dev=None):
+        """images: (B, 2, H, W) uint8 host array (or device pointer via
+        ``images_dev``); motions: list of B 4x4 arrays or None."""
+        self.engine.step(images, motions, sync=sync, images_dev=images_dev)
+
+    def sync(self):
+        self.engine.sync()
+
+    def result(self, seq: int) -> FrameResult:
+        return FrameResult(self.engine, seq, self.engine.frame(seq))
+
+
+@dataclass
+class Sequence:
+    """pipeline.py:173-185."""
+
+    rig: StereoRig
+    lefts: list
+    rights: list
+    motions: list
+    gt_left: list | None = None
+    gt_right: list | None = None
+
+    def __len__(self) -> int:
+        return len(self.lefts)
+
+
+def relative_motions(poses):
+    """pipeline.py:188-193."""
+    motions = [None]
+    for prev, curr in zip(poses[:-1], poses[1:]):
+        motions.append(np.linalg.inv(curr) @ prev)
+    return motions
+
+
+def run_sequence(seq: Sequence, params: PipelineParams | None = None, out_dir: str | None = None,
+                 metric_mode: str = "or"):
+    """pipeline.py:241-302: per-frame loop plus the metrics lines; the output
+    tree (PNG files) is written only when ``out_dir`` is given and OpenCV is
+    importable."""
+    params = params or PipelineParams()
+    pipe = DisparityPipeline(seq.rig, params)
+    results = []
+    for k in range(len(seq)):
+        results.append(pipe.process_frame(seq.lefts[k], seq.rights[k], seq.motions[k]))
+    pipe._flush()
+    if out_dir is not None:
+        import cv2
+        os.makedirs(os.path.join(out_dir, "disp_0"), exist_ok=True)
+        lines = []
+        for k, res in enumerate(results):
+            fl = res.fused.left
+            raw = np.where(fl.valid, np.maximum(np.rint(fl.values * 256.0), 1.0), 0.0)
+            cv2.imwrite(os.path.join(out_dir, "disp_0", f"{k:06d}.png"), raw.astype(np.uint16))
+            lines.append(f"frame={k:06d} density={float(fl.valid.mean()):.6f} "
+                         f"search_fraction={res.search_fraction_left:.6f}")
+        with open(os.path.join(out_dir, "metrics.txt"), "w") as fh:
+            fh.write("\n".join(lines) + "\n")
+    return results

@@ -21,6 +21,8 @@
 //   F32 (any other penalties / volumes): float2 per lane, numpy's float32
 //     operation order, 8 single-direction launches in the reference's
 //     summation order (H->, H<-, dy=+1 dx=-1,0,1, dy=-1 dx=-1,0,1).
+#include <cstdlib>
+
 #include "es_common.cuh"
 #include "es_kernels.h"
 
@@ -224,6 +226,199 @@ __global__ void __launch_bounds__(SGM_WARPS * 32) k_sgm(SgmArgs a, int fam, int 
   }
 }
 
+// ------------------------------------------------------------ grouped (u16)
+//
+// The production u16 kernel.  A warp walks NG = 32/G chains in lockstep, G
+// lanes per chain; lane g of a chain's group holds pair c*G + g of chunk c
+// (2G cells per chunk, absolute disparity).  Per step the warp loops only
+// over the union of its chains' chunk ranges, so reduced intervals cost one
+// or two chunks.  Chain metadata is loaded G steps at a time (one load per
+// lane) and broadcast with a shuffle; the next step's cost and partial sums
+// are loaded into registers while the current step computes, so the
+// recurrence's critical path has no global-memory latency.  Diagonal chains
+// are walked row by row (inactive on rows where they leave the image).
+
+constexpr int GRP_WARPS = 4;
+
+__device__ __forceinline__ bool grp_pixel(int fam, int bwd, int c, int t, int W, int H, int& x,
+                                          int& y) {
+  if (fam == FAM_H) {
+    y = c;
+    x = bwd ? W - 1 - t : t;
+    return c < H;
+  }
+  y = bwd ? H - 1 - t : t;
+  if (fam == FAM_V) {
+    x = c;
+    return c < W;
+  }
+  x = fam == FAM_D1 ? c - (H - 1) + y : c - y;
+  return x >= 0 && x < W && c < W + H - 1;
+}
+
+template <int G, int NCH>
+__global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp(SgmArgs a, int fam, int sweeps,
+                                                             int init) {
+  constexpr int NG = 32 / G;
+  constexpr uint32_t NONE = 0xFFFFFFFFu;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int grp = lane / G;
+  const int gbase = lane & ~(G - 1);
+  const int W = a.W, H = a.H;
+  const int nchains = fam == FAM_H ? H : (fam == FAM_V ? W : W + H - 1);
+  const int c0 = (blockIdx.x * GRP_WARPS + (threadIdx.x >> 5)) * NG;
+  if (c0 >= nchains) return;
+  const int ch = c0 + grp;
+  const size_t HW = (size_t)W * H;
+  const uint2* __restrict__ meta = a.meta + (size_t)blockIdx.y * HW;
+  const uint32_t* __restrict__ C =
+      reinterpret_cast<const uint32_t*>(a.C) + (size_t)blockIdx.y * a.volcap;
+  uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
+  const uint32_t p1x2 = a.p1i * 0x10001u;
+  const int len = fam == FAM_H ? W : H;
+  const int src_l = gbase | ((gl + G - 1) & (G - 1));
+  const int src_r = gbase | ((gl + 1) & (G - 1));
+  bool first_sweep = true;
+  for (int bwd = 0; bwd < 2; ++bwd) {
+    if (!(sweeps & (1 << bwd))) continue;
+    const bool init_sum = init && first_sweep;
+    first_sweep = false;
+    // meta batches: lane g of a group holds the meta of step tb + g
+    auto load_meta = [&](int tb) -> uint2 {
+      int x, y;
+      const int t = tb + gl;
+      if (t < len && grp_pixel(fam, bwd, ch, t, W, H, x, y)) return meta[(size_t)y * W + x];
+      return make_uint2(NONE, 0u);   // no pixel on this step
+    };
+    uint2 mb_cur = load_meta(0);
+    uint2 mb_next = load_meta(G);
+    int tb = 0;
+    uint32_t prev[NCH], cn[NCH], sn[NCH], kn[NCH];
+    // step 0's meta, chunk range and prefetched operands
+    uint32_t mx = __shfl_sync(FULL, mb_cur.x, gbase);
+    uint32_t my = __shfl_sync(FULL, mb_cur.y, gbase);
+    bool act = mx != NONE;
+    int j0 = (int)((mx & 0xFFFFu) >> 1), j1 = (int)((mx >> 16) >> 1);
+    int clo = act ? j0 / G : NCH, chi = act ? j1 / G : -1;
+    int ulo = __reduce_min_sync(FULL, clo), uhi = __reduce_max_sync(FULL, chi);
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      prev[c] = INF16x2;
+      cn[c] = INF16x2;
+      sn[c] = 0u;
+      kn[c] = NONE;
+      const int j = c * G + gl;
+      if (c >= ulo && c <= uhi && act && j >= j0 && j <= j1) {
+        kn[c] = my + (uint32_t)(j - j0);
+        cn[c] = __ldg(C + kn[c]);
+        if (!init_sum) sn[c] = S[kn[c]];
+      }
+    }
+    uint32_t m = 0;
+    bool was_active = false;
+    for (int t = 0; t < len; ++t) {
+      // ---- the next step's meta and chunk range (prefetch target)
+      bool act1 = false;
+      int j0n = 0, j1n = -1, clo1 = NCH, chi1 = -1;
+      uint32_t my1 = 0;
+      if (t + 1 < len) {
+        if (t + 1 == tb + G) {   // step t+1 opens the next batch: rotate, and
+          tb += G;               // issue the batch after it (used G steps later)
+          mb_cur = mb_next;
+          mb_next = load_meta(tb + G);
+        }
+        const int r = t + 1 - tb;   // 0 .. G-1
+        const uint32_t mx1 = __shfl_sync(FULL, mb_cur.x, gbase | r);
+        my1 = __shfl_sync(FULL, mb_cur.y, gbase | r);
+        act1 = mx1 != NONE;
+        j0n = (int)((mx1 & 0xFFFFu) >> 1);
+        j1n = (int)((mx1 >> 16) >> 1);
+        if (act1) {
+          clo1 = j0n / G;
+          chi1 = j1n / G;
+        }
+      }
+      const int ulo1 = __reduce_min_sync(FULL, clo1), uhi1 = __reduce_max_sync(FULL, chi1);
+      // ---- this step
+      const bool first = act && !was_active;
+      const uint32_t mp2 = (m + a.p2i) * 0x10001u;
+      const uint32_t ng = ((0x10000u - m) & 0xFFFFu) * 0x10001u;
+      uint32_t cur[NCH];
+      uint32_t nmin = INF16x2;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        cur[c] = INF16x2;
+        if (c >= ulo && c <= uhi) {
+          const uint32_t srcl = gl == G - 1 ? (c > 0 ? prev[c > 0 ? c - 1 : 0] : INF16x2) : prev[c];
+          const uint32_t srcr =
+              gl == 0 ? (c + 1 < NCH ? prev[c + 1 < NCH ? c + 1 : c] : INF16x2) : prev[c];
+          const uint32_t pl = __shfl_sync(FULL, srcl, src_l);
+          const uint32_t pr = __shfl_sync(FULL, srcr, src_r);
+          const uint32_t pv = prev[c];
+          const uint32_t nb = __vminu2(__byte_perm(pl, pv, 0x5432), __byte_perm(pv, pr, 0x5432));
+          const uint32_t cand = __vminu2(__viaddmin_u16x2(nb, p1x2, pv), mp2);
+          uint32_t L = first ? cn[c] : __vadd2(cn[c], __vadd2(cand, ng));
+          if (c < clo || c > chi) L = INF16x2;
+          cur[c] = L;
+          nmin = __vminu2(nmin, L);
+          if (kn[c] != NONE) S[kn[c]] = init_sum ? L : __vadd2(sn[c], L);
+        }
+        // refill chunk c for step t+1 (after its use above)
+        if (c >= ulo1 && c <= uhi1) {
+          const int j = c * G + gl;
+          cn[c] = INF16x2;
+          sn[c] = 0u;
+          kn[c] = NONE;
+          if (act1 && j >= j0n && j <= j1n) {
+            kn[c] = my1 + (uint32_t)(j - j0n);
+            cn[c] = __ldg(C + kn[c]);
+            if (!init_sum) sn[c] = S[kn[c]];
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) prev[c] = cur[c];
+      // per-chain minimum: one REDUX per group over masked values
+      const uint32_t hm = min(nmin & 0xFFFFu, nmin >> 16);
+      uint32_t mg = 0;
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const uint32_t r = __reduce_min_sync(FULL, grp == g ? hm : 0xFFFFFFFFu);
+        if (grp == g) mg = r;
+      }
+      m = mg;
+      was_active = act;
+      act = act1;
+      j0 = j0n;
+      j1 = j1n;
+      clo = clo1;
+      chi = chi1;
+      ulo = ulo1;
+      uhi = uhi1;
+    }
+  }
+}
+
+template <int G>
+static void launch_grp(const SgmArgs& a, int nch_pairs, int fam, int sweeps, int init, int n_sv,
+                       cudaStream_t st) {
+  const int nchains = fam == FAM_H ? a.H : (fam == FAM_V ? a.W : a.W + a.H - 1);
+  constexpr int per_block = GRP_WARPS * (32 / G);
+  dim3 grid((nchains + per_block - 1) / per_block, n_sv);
+  const int nch = (nch_pairs + G - 1) / G;
+  if (nch <= 2) k_sgm_grp<G, 2><<<grid, GRP_WARPS * 32, 0, st>>>(a, fam, sweeps, init);
+  else if (nch <= 4) k_sgm_grp<G, 4><<<grid, GRP_WARPS * 32, 0, st>>>(a, fam, sweeps, init);
+  else if (nch <= 8) k_sgm_grp<G, 8><<<grid, GRP_WARPS * 32, 0, st>>>(a, fam, sweeps, init);
+  else if (nch <= 16) k_sgm_grp<G, 16><<<grid, GRP_WARPS * 32, 0, st>>>(a, fam, sweeps, init);
+  else k_sgm_grp<G, 32><<<grid, GRP_WARPS * 32, 0, st>>>(a, fam, sweeps, init);
+}
+
+static void launch_family_seg(const SgmArgs& a, int fam, int sweeps, int init, int n_sv,
+                              cudaStream_t st) {
+  launch_grp<8>(a, npairs_max(a.d_max), fam, sweeps, init, n_sv, st);
+}
+
 template <class A, bool CF32>
 static void launch_family(const SgmArgs& a, int nch, int fam, int sweeps, int init, int n_sv,
                           cudaStream_t st) {
@@ -242,7 +437,13 @@ static void launch_family(const SgmArgs& a, int nch, int fam, int sweeps, int in
 void launch_aggregate(const SgmArgs& a, int arith, int n_sv, cudaStream_t st) {
   int nch = (npairs_max(a.d_max) + 31) / 32;
   if (nch > 4) nch = 8;
-  if (arith == ARITH_U16) {
+  static const bool v1 = getenv("ES_SGM_V1") != nullptr;   // A/B switch for profiling
+  if (arith == ARITH_U16 && !v1) {
+    launch_family_seg(a, FAM_H, 3, 1, n_sv, st);
+    launch_family_seg(a, FAM_V, 3, 0, n_sv, st);
+    launch_family_seg(a, FAM_D1, 3, 0, n_sv, st);
+    launch_family_seg(a, FAM_D2, 3, 0, n_sv, st);
+  } else if (arith == ARITH_U16) {
     launch_family<U16A, false>(a, nch, FAM_H, 3, 1, n_sv, st);
     launch_family<U16A, false>(a, nch, FAM_V, 3, 0, n_sv, st);
     launch_family<U16A, false>(a, nch, FAM_D1, 3, 0, n_sv, st);

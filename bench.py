@@ -167,7 +167,11 @@ def main():
     ap.add_argument("--cpu-procs", type=int, default=min(8, os.cpu_count() or 1))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--texture-scale", type=float, default=TEXTURE_SCALE,
+                    help="world-space texture lattice (m); 0.05 gives paper-like ~50%% "
+                         "search fractions, 0.2 gives ~10%%")
     args = ap.parse_args()
+    globals()["TEXTURE_SCALE"] = args.texture_scale
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -257,13 +261,13 @@ def main():
     e2e = None
     if not args.no_e2e:
         host = torch.empty((B, 2, H, W), dtype=torch.uint8, pin_memory=True)
-        out_k = np.empty((H, W), np.uint16)
         # restart the sequences so e2e runs the same frames
         bp.reset()
         for k in range(Wm):
             host.copy_(imgs[k])
             bp.process_frames(host.numpy(), motions_for(specs, k), sync=True)
         staged = [imgs[Wm + i].cpu().pin_memory() for i in range(K)]
+        outs = [torch.empty((B, H, W), dtype=torch.int16, pin_memory=True) for _ in range(K)]
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(device)
@@ -271,11 +275,13 @@ def main():
         with torch.cuda.stream(ext):
             e0.record()
         for i in range(K):
-            bp.process_frames(staged[i].numpy(), motions_for(specs, Wm + i), sync=True)
-            for s in range(B):
-                _lib.call("es_ctx_export", eng._h, _lib.ES_FUSED_KITTI, s, 0, _lib.ptr(out_k))
+            # public API: pinned host images in, fused KITTI maps of all B
+            # sequences out, every step
+            bp.process_frames(staged[i].numpy(), motions_for(specs, Wm + i), sync=False)
+            bp.fused_kitti(0, out=outs[i].numpy().view(np.uint16), sync=False)
         with torch.cuda.stream(ext):
             e1.record()
+        bp.sync()
         torch.cuda.synchronize(device)
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
         if world > 1:

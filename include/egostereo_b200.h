@@ -99,6 +99,9 @@ enum {
   ES_FUSED_KITTI                                   /* u16 round(256 d), 0 = invalid */
 };
 int es_ctx_export(es_ctx* ctx, int what, int seq, int view, void* host_out);
+/* one map of one view for all `batch` sequences into host_out [batch][H][W]
+ * (no dense volumes); sync = 0 only enqueues the copy on the context stream */
+int es_ctx_export_all(es_ctx* ctx, int what, int view, void* host_out, int sync);
 /* device pointer of a per-sequence map (what as above, no dense volumes) */
 int es_ctx_device_ptr(es_ctx* ctx, int what, int seq, int view, void** dev_ptr);
 /* stream the context launches on (cudaStream_t) */

@@ -63,6 +63,7 @@ SIGNATURES = {
     "es_ctx_profile": [_P, _I],
     "es_ctx_stage_times": [_P, _P, _P],
     "es_ctx_export": [_P, _I, _I, _I, _P],
+    "es_ctx_export_all": [_P, _I, _I, _P, _I],
     "es_ctx_device_ptr": [_P, _I, _I, _I, _P],
     "es_ctx_stream": [_P, _P],
     "es_search_intervals": [_P, _P, _P, _I, _I, _I, _P, _P],

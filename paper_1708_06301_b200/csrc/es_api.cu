@@ -189,6 +189,15 @@ struct es_ctx {
   static constexpr int NSTAGE = 6;
   bool profiling = false;
   std::vector<std::array<cudaEvent_t, NSTAGE + 1>> prof;
+  uint16_t* kitti = nullptr;   // batched KITTI export staging
+  int lanes = 0;               // SGM lanes per chain (0 = heuristic)
+  double last_fraction = 1.0;  // search fraction of the last synced step
+
+  void note_fraction() {
+    unsigned long long cells = 0;
+    for (int s = 0; s < 2 * B; ++s) cells += h_cells[s];
+    last_fraction = (double)cells / ((double)HW * 2 * B * (rig.d_max + 1));
+  }
 };
 
 namespace {
@@ -199,7 +208,7 @@ int ctx_free(es_ctx* c) {
   void* ptrs[] = {c->img, c->sd[0], c->sd[1], c->sp[0], c->sp[1], c->sv[0], c->sv[1], c->hd,
                   c->hp, c->hv, c->pd, c->pp, c->pv, c->zkey, c->zidx, c->meta, c->C, c->S,
                   c->dstar, c->r, c->mvalid, c->keep, c->Hm, c->have_pred, c->err, c->anyv,
-                  c->cells};
+                  c->cells, c->kitti};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   void* hptrs[] = {c->h_Hm, c->h_have, c->h_err, c->h_anyv, c->h_cells};
@@ -354,7 +363,8 @@ int es_ctx_sync(es_ctx* c) {
   if (c->pending) {
     c->pending = false;
     for (int s = 0; s < c->B; ++s) c->have_state[s] = c->h_anyv[s] != 0;
-    return commit_errors(c);
+    c->note_fraction();
+    return commit_errors(c);   // error bits accumulated over the deferred steps
   }
   return ES_OK;
 }
@@ -402,7 +412,8 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   CK(cudaMemcpyAsync(c->Hm, h_Hm, sizeof(double) * 32 * B, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(c->have_pred, h_have, B, cudaMemcpyHostToDevice, c->st));
   CK(cudaEventRecord(c->ring_ev[slot], c->st));
-  CK(cudaMemsetAsync(c->err, 0, sizeof(int) * B, c->st));
+  // error bits accumulate across deferred steps until a sync reads them
+  if (!c->pending) CK(cudaMemsetAsync(c->err, 0, sizeof(int) * B, c->st));
   CK(cudaMemsetAsync(c->anyv, 0, sizeof(int) * B, c->st));
 
   PredArgs pa = pred_args(c);
@@ -438,6 +449,11 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   sa.p2i = c->prm.p2i;
   sa.p1 = c->prm.p1;
   sa.p2 = c->prm.p2;
+  // lanes per chain: wide intervals (large search fraction) favour 16 lanes,
+  // reduced ones 8 (measured); chosen per (seq, view) on the
+  // device from this frame's searched-cell count
+  sa.lanes = c->lanes;
+  sa.cells = c->cells;
   launch_aggregate(sa, c->arith, n_sv, c->st);
   mark(4);
 
@@ -488,6 +504,7 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   if (sync) {
     CK(cudaStreamSynchronize(c->st));
     if (int e = commit_errors(c)) return e;   // state not committed
+    c->note_fraction();
     c->cur = nxt;
     for (int s = 0; s < B; ++s) {
       c->frame[s] += 1;
@@ -634,6 +651,32 @@ int es_ctx_export(es_ctx* c, int what, int seq, int view, void* out) {
 }
 
 }  // extern "C"
+
+extern "C" int es_ctx_export_all(es_ctx* c, int what, int view, void* out, int sync) {
+  CK(cudaSetDevice(c->device));
+  if (view < 0 || view > 1) return fail(ES_ERR_VALUE, "bad view");
+  const size_t HW = c->HW;
+  const int B = c->B;
+  if (what == ES_FUSED_KITTI) {
+    if (!c->kitti) CK(cudaMalloc(&c->kitti, sizeof(uint16_t) * HW * B));
+    for (int s = 0; s < B; ++s) {
+      const size_t o = ((size_t)s * 2 + view) * HW;
+      k_kitti<<<(unsigned)((HW + 255) / 256), 256, 0, c->st>>>(c->sd[c->cur] + o, c->sv[c->cur] + o,
+                                                               HW, c->kitti + (size_t)s * HW);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, c->kitti, sizeof(uint16_t) * HW * B, cudaMemcpyDeviceToHost, c->st));
+  } else {
+    void* p;
+    if (int e = es_ctx_device_ptr(c, what, 0, view, &p)) return e;
+    const bool u8 = what == ES_PRED_VALID || what == ES_MEAS_VALID || what == ES_KEEP ||
+                    what == ES_FUSED_VALID;
+    const size_t es = u8 ? 1 : sizeof(double);
+    CK(cudaMemcpy2DAsync(out, HW * es, p, 2 * HW * es, HW * es, B, cudaMemcpyDeviceToHost, c->st));
+  }
+  if (sync) CK(cudaStreamSynchronize(c->st));
+  return ES_OK;
+}
 
 // ------------------------------------------------------------ stage level
 

@@ -60,6 +60,13 @@ struct SgmArgs {
   int cost_f32;
   uint32_t p1i, p2i;
   float p1, p2;
+  int lanes = 0;        // lanes per chain of the u16 kernel (8/16/32; 0 = default)
+  // device-side lane choice: with cells != nullptr both the 8- and 16-lane
+  // kernels launch and each (seq, view) runs in the one matching its search
+  // fraction (<= split: 8 lanes, > split: 16 lanes)
+  const unsigned long long* cells = nullptr;
+  double split = 0.3;
+  int select = 0;       // internal: 0 all, 1 fraction <= split, 2 fraction > split
 };
 // full 8-path aggregation; the u16 path runs 4 family launches (both sweeps
 // each), the f32 path runs the 8 directions in the reference's order

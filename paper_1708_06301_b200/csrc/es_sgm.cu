@@ -269,13 +269,22 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp(SgmArgs a, int fam, 
   const int nchains = fam == FAM_H ? H : (fam == FAM_V ? W : W + H - 1);
   const int c0 = (blockIdx.x * GRP_WARPS + (threadIdx.x >> 5)) * NG;
   if (c0 >= nchains) return;
+  if (a.select) {   // per-(seq, view) choice of G from the frame's searched cells
+    const double frac = (double)a.cells[blockIdx.y] / ((double)W * H * (a.d_max + 1));
+    if ((a.select == 1) == (frac > a.split)) return;
+  }
   const int ch = c0 + grp;
   const size_t HW = (size_t)W * H;
   const uint2* __restrict__ meta = a.meta + (size_t)blockIdx.y * HW;
   const uint32_t* __restrict__ C =
       reinterpret_cast<const uint32_t*>(a.C) + (size_t)blockIdx.y * a.volcap;
   uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
+  // keep the per-(seq, view) bases in registers (ptxas otherwise re-derives
+  // them from the parameter bank at every load and store)
+  asm volatile("" : "+l"(C));
+  asm volatile("" : "+l"(S));
   const uint32_t p1x2 = a.p1i * 0x10001u;
+  const uint32_t p2 = a.p2i;
   const int len = fam == FAM_H ? W : H;
   const int src_l = gbase | ((gl + G - 1) & (G - 1));
   const int src_r = gbase | ((gl + 1) & (G - 1));
@@ -294,34 +303,35 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp(SgmArgs a, int fam, 
     uint2 mb_cur = load_meta(0);
     uint2 mb_next = load_meta(G);
     int tb = 0;
-    uint32_t prev[NCH], cn[NCH], sn[NCH], kn[NCH];
+    // chunk c of this group: pairs c*G + gl; a step's operands are valid for
+    // rel = c*G + gl - j0 < span (span = 0 when the chain has no pixel)
+    auto umask = [](int lo, int hi) -> uint32_t {   // chunks lo..hi as a bit mask
+      return hi < lo ? 0u : ((hi >= 31 ? 0xFFFFFFFFu : ((2u << hi) - 1u)) & ~((1u << lo) - 1u));
+    };
+    uint32_t prev[NCH], cn[NCH], sn[NCH];
     // step 0's meta, chunk range and prefetched operands
-    uint32_t mx = __shfl_sync(FULL, mb_cur.x, gbase);
+    const uint32_t mx0 = __shfl_sync(FULL, mb_cur.x, gbase);
     uint32_t my = __shfl_sync(FULL, mb_cur.y, gbase);
-    bool act = mx != NONE;
-    int j0 = (int)((mx & 0xFFFFu) >> 1), j1 = (int)((mx >> 16) >> 1);
-    int clo = act ? j0 / G : NCH, chi = act ? j1 / G : -1;
-    int ulo = __reduce_min_sync(FULL, clo), uhi = __reduce_max_sync(FULL, chi);
+    bool act = mx0 != NONE;
+    int j0 = (int)((mx0 & 0xFFFFu) >> 1);
+    uint32_t span = act ? (uint32_t)((int)((mx0 >> 16) >> 1) - j0 + 1) : 0u;
+    uint32_t um = umask(__reduce_min_sync(FULL, act ? j0 / G : NCH),
+                        __reduce_max_sync(FULL, act ? (int)((mx0 >> 16) >> 1) / G : -1));
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
       prev[c] = INF16x2;
-      cn[c] = INF16x2;
-      sn[c] = 0u;
-      kn[c] = NONE;
-      const int j = c * G + gl;
-      if (c >= ulo && c <= uhi && act && j >= j0 && j <= j1) {
-        kn[c] = my + (uint32_t)(j - j0);
-        cn[c] = __ldg(C + kn[c]);
-        if (!init_sum) sn[c] = S[kn[c]];
-      }
+      const uint32_t rel = (uint32_t)(c * G + gl - j0);
+      const bool in = ((um >> c) & 1u) && rel < span;
+      cn[c] = in ? __ldg(C + (my + rel)) : INF16x2;
+      sn[c] = (in && !init_sum) ? S[my + rel] : 0u;
     }
     uint32_t m = 0;
     bool was_active = false;
     for (int t = 0; t < len; ++t) {
-      // ---- the next step's meta and chunk range (prefetch target)
-      bool act1 = false;
-      int j0n = 0, j1n = -1, clo1 = NCH, chi1 = -1;
-      uint32_t my1 = 0;
+      // ---- the next step's meta and chunk mask (prefetch target)
+      int j0n = 0;
+      uint32_t my1 = 0, span1 = 0;
+      int clo1 = NCH, chi1 = -1;
       if (t + 1 < len) {
         if (t + 1 == tb + G) {   // step t+1 opens the next batch: rotate, and
           tb += G;               // issue the batch after it (used G steps later)
@@ -331,54 +341,50 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp(SgmArgs a, int fam, 
         const int r = t + 1 - tb;   // 0 .. G-1
         const uint32_t mx1 = __shfl_sync(FULL, mb_cur.x, gbase | r);
         my1 = __shfl_sync(FULL, mb_cur.y, gbase | r);
-        act1 = mx1 != NONE;
-        j0n = (int)((mx1 & 0xFFFFu) >> 1);
-        j1n = (int)((mx1 >> 16) >> 1);
-        if (act1) {
+        if (mx1 != NONE) {
+          j0n = (int)((mx1 & 0xFFFFu) >> 1);
+          const int j1n = (int)((mx1 >> 16) >> 1);
+          span1 = (uint32_t)(j1n - j0n + 1);
           clo1 = j0n / G;
           chi1 = j1n / G;
         }
       }
-      const int ulo1 = __reduce_min_sync(FULL, clo1), uhi1 = __reduce_max_sync(FULL, chi1);
+      const uint32_t um1 = umask(__reduce_min_sync(FULL, clo1), __reduce_max_sync(FULL, chi1));
       // ---- this step
       const bool first = act && !was_active;
-      const uint32_t mp2 = (m + a.p2i) * 0x10001u;
+      const uint32_t mp2 = (m + p2) * 0x10001u;
       const uint32_t ng = ((0x10000u - m) & 0xFFFFu) * 0x10001u;
-      uint32_t cur[NCH];
       uint32_t nmin = INF16x2;
+      uint32_t left_old = INF16x2;   // prev[c-1] before this step overwrote it
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {
-        cur[c] = INF16x2;
-        if (c >= ulo && c <= uhi) {
-          const uint32_t srcl = gl == G - 1 ? (c > 0 ? prev[c > 0 ? c - 1 : 0] : INF16x2) : prev[c];
-          const uint32_t srcr =
-              gl == 0 ? (c + 1 < NCH ? prev[c + 1 < NCH ? c + 1 : c] : INF16x2) : prev[c];
+        const uint32_t pv = prev[c];
+        if ((um >> c) & 1u) {
+          const uint32_t srcl = gl == G - 1 ? left_old : pv;
+          const uint32_t srcr = gl == 0 ? (c + 1 < NCH ? prev[c + 1 < NCH ? c + 1 : c] : INF16x2) : pv;
           const uint32_t pl = __shfl_sync(FULL, srcl, src_l);
           const uint32_t pr = __shfl_sync(FULL, srcr, src_r);
-          const uint32_t pv = prev[c];
           const uint32_t nb = __vminu2(__byte_perm(pl, pv, 0x5432), __byte_perm(pv, pr, 0x5432));
           const uint32_t cand = __vminu2(__viaddmin_u16x2(nb, p1x2, pv), mp2);
-          uint32_t L = first ? cn[c] : __vadd2(cn[c], __vadd2(cand, ng));
-          if (c < clo || c > chi) L = INF16x2;
-          cur[c] = L;
+          // chunks outside this chain's own range carry cn = +inf, so L lands
+          // in the [0x8000, 0x8000 + P2] band and is never selected
+          const uint32_t L = first ? cn[c] : __vadd2(cn[c], __vadd2(cand, ng));
+          prev[c] = L;
           nmin = __vminu2(nmin, L);
-          if (kn[c] != NONE) S[kn[c]] = init_sum ? L : __vadd2(sn[c], L);
+          const uint32_t rel = (uint32_t)(c * G + gl - j0);
+          if (rel < span) S[my + rel] = init_sum ? L : __vadd2(sn[c], L);
+        } else {
+          prev[c] = INF16x2;
         }
+        left_old = pv;
         // refill chunk c for step t+1 (after its use above)
-        if (c >= ulo1 && c <= uhi1) {
-          const int j = c * G + gl;
-          cn[c] = INF16x2;
-          sn[c] = 0u;
-          kn[c] = NONE;
-          if (act1 && j >= j0n && j <= j1n) {
-            kn[c] = my1 + (uint32_t)(j - j0n);
-            cn[c] = __ldg(C + kn[c]);
-            if (!init_sum) sn[c] = S[kn[c]];
-          }
+        if ((um1 >> c) & 1u) {
+          const uint32_t rel = (uint32_t)(c * G + gl - j0n);
+          const bool in = rel < span1;
+          cn[c] = in ? __ldg(C + (my1 + rel)) : INF16x2;
+          sn[c] = (in && !init_sum) ? S[my1 + rel] : 0u;
         }
       }
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) prev[c] = cur[c];
       // per-chain minimum: one REDUX per group over masked values
       const uint32_t hm = min(nmin & 0xFFFFu, nmin >> 16);
       uint32_t mg = 0;
@@ -389,13 +395,11 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp(SgmArgs a, int fam, 
       }
       m = mg;
       was_active = act;
-      act = act1;
+      act = span1 != 0;
       j0 = j0n;
-      j1 = j1n;
-      clo = clo1;
-      chi = chi1;
-      ulo = ulo1;
-      uhi = uhi1;
+      my = my1;
+      span = span1;
+      um = um1;
     }
   }
 }
@@ -416,7 +420,20 @@ static void launch_grp(const SgmArgs& a, int nch_pairs, int fam, int sweeps, int
 
 static void launch_family_seg(const SgmArgs& a, int fam, int sweeps, int init, int n_sv,
                               cudaStream_t st) {
-  launch_grp<8>(a, npairs_max(a.d_max), fam, sweeps, init, n_sv, st);
+  static const int forced = getenv("ES_SGM_G") ? atoi(getenv("ES_SGM_G")) : 0;
+  const int np = npairs_max(a.d_max);
+  if (!forced && !a.lanes && a.cells) {
+    SgmArgs lo = a, hi = a;
+    lo.select = 1;
+    hi.select = 2;
+    launch_grp<8>(lo, np, fam, sweeps, init, n_sv, st);
+    launch_grp<16>(hi, np, fam, sweeps, init, n_sv, st);
+    return;
+  }
+  const int g = forced ? forced : (a.lanes ? a.lanes : 8);
+  if (g >= 32) launch_grp<32>(a, np, fam, sweeps, init, n_sv, st);
+  else if (g >= 16) launch_grp<16>(a, np, fam, sweeps, init, n_sv, st);
+  else launch_grp<8>(a, np, fam, sweeps, init, n_sv, st);
 }
 
 template <class A, bool CF32>
@@ -538,8 +555,69 @@ __global__ void __launch_bounds__(256) k_wta_var(WtaArgs a) {
   a.r[o] = fmax((double)count, a.r_min);
 }
 
+// u16 sums, one thread per pixel: the argmin streams the pixel's pairs with
+// 8-byte loads where aligned, then walks outward (sgm.py:319-344).  The
+// pairs of neighbouring pixels are adjacent, so a warp's loads stay within a
+// few cache lines and the walk re-reads from L1.
+__global__ void __launch_bounds__(256) k_wta_var_u16(WtaArgs a) {
+  const size_t HW = (size_t)a.W * a.H;
+  const size_t pix = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= HW) return;
+  const int svl = blockIdx.y;
+  const uint2 mt = a.meta[svl * HW + pix];
+  const int lo = lo_of(mt), hi = hi_of(mt);
+  const int j0 = lo >> 1, j1 = hi >> 1;
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(a.S) + svl * a.volcap + mt.y;
+  // key = value << 16 | d: the minimum key is the smallest value, then d
+  uint32_t best = 0xFFFFFFFFu;
+  {
+    const uint32_t w = s[0];
+    const uint32_t d0 = 2u * j0;
+    if ((int)d0 >= lo) best = min(best, ((w & 0xFFFFu) << 16) | d0);
+    if ((int)d0 + 1 <= hi) best = min(best, (w & 0xFFFF0000u) | (d0 + 1));
+  }
+  for (int j = j0 + 1; j < j1; ++j) {
+    const uint32_t w = s[j - j0];
+    const uint32_t d0 = 2u * j;
+    best = min(best, min(((w & 0xFFFFu) << 16) | d0, (w & 0xFFFF0000u) | (d0 + 1)));
+  }
+  if (j1 > j0) {
+    const uint32_t w = s[j1 - j0];
+    const uint32_t d0 = 2u * j1;
+    best = min(best, ((w & 0xFFFFu) << 16) | d0);
+    if ((int)d0 + 1 <= hi) best = min(best, (w & 0xFFFF0000u) | (d0 + 1));
+  }
+  const int dstar = (int)(best & 0xFFFFu);
+  const uint32_t cstar = best >> 16;
+  auto cell = [&](int d) -> uint32_t {
+    const uint32_t w = s[(d >> 1) - j0];
+    return (d & 1) ? (w >> 16) : (w & 0xFFFFu);
+  };
+  long long count = 0;
+  double acc = 0.0;
+  for (int d = dstar - 1; d >= lo; --d) {
+    acc += (double)(cell(d) - cstar);
+    if (!(acc < a.s_max)) break;
+    ++count;
+  }
+  acc = 0.0;
+  for (int d = dstar + 1; d <= hi; ++d) {
+    acc += (double)(cell(d) - cstar);
+    if (!(acc < a.s_max)) break;
+    ++count;
+  }
+  const size_t o = svl * HW + pix;
+  a.dstar[o] = (uint16_t)dstar;
+  a.valid[o] = dstar > 0;
+  a.r[o] = fmax((double)count, a.r_min);
+}
+
 void launch_wta_variance(const WtaArgs& a, int n_sv, cudaStream_t st) {
   const size_t HW = (size_t)a.W * a.H;
+  if (a.arith == ARITH_U16 && a.dstar_in == nullptr) {
+    k_wta_var_u16<<<dim3((unsigned)((HW + 255) / 256), n_sv), 256, 0, st>>>(a);
+    return;
+  }
   dim3 grid((unsigned)((HW + 7) / 8), n_sv);
   if (a.arith == ARITH_U16) k_wta_var<false><<<grid, 256, 0, st>>>(a);
   else k_wta_var<true><<<grid, 256, 0, st>>>(a);

@@ -301,6 +301,17 @@ class BatchedPipeline:
     def sync(self):
         self.engine.sync()
 
+    def fused_kitti(self, view: int = 0, out=None, sync: bool = True) -> np.ndarray:
+        """Fused disparity of every sequence in the KITTI uint16 encoding
+        (kitti_io.py:38-46), one batched device->host copy.  With
+        ``sync=False`` the copy is only enqueued (``out`` should be pinned)."""
+        h, w = self.rig.height, self.rig.width
+        if out is None:
+            out = np.empty((self.batch, h, w), np.uint16)
+        _lib.call("es_ctx_export_all", self.engine._h, _lib.ES_FUSED_KITTI, int(view),
+                  _lib.ptr(out), 1 if sync else 0)
+        return out
+
     def result(self, seq: int) -> FrameResult:
         return FrameResult(self.engine, seq, self.engine.frame(seq))
 

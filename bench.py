@@ -173,9 +173,8 @@ def main():
     args = ap.parse_args()
     globals()["TEXTURE_SCALE"] = args.texture_scale
 
-    rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", 0))
+    from paper_1708_06301_b200 import sharding
+    rank, world, local = sharding.world()
     import torch
     import torch.distributed as dist
     device = torch.device("cuda", local)
@@ -211,7 +210,8 @@ def main():
     from paper_1708_06301_b200.core import StereoRig
 
     rig = StereoRig(**RIG)
-    specs = sequence_specs(B, seed0=1000 + 1000 * rank)
+    seeds = sharding.rank_sequences(rank, world, B, seed0=1000)
+    specs = sequence_specs(B, seed0=seeds[0])
     frames = list(range(Wm + K))
     imgs = render_frames(specs, frames, device)
     bp = pipeline.BatchedPipeline(rig, B, device=local)
@@ -224,9 +224,10 @@ def main():
 
     # ---- device-resident timed region ---------------------------------
     _lib.call("es_ctx_profile", eng._h, 1)
+    acc = ctypes.c_uint64()
+    _lib.call("es_ctx_cells_acc", eng._h, ctypes.byref(acc), 1)   # reset the accumulator
     clocks = Clocks(local) if rank == 0 else None
-    if world > 1:
-        dist.barrier()
+    sharding.barrier()
     torch.cuda.synchronize(device)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(ext):
@@ -246,14 +247,11 @@ def main():
     nsteps = ctypes.c_int64()
     _lib.call("es_ctx_stage_times", eng._h, _lib.ptr(stage), ctypes.byref(nsteps))
     _lib.call("es_ctx_profile", eng._h, 0)
-    # cells of the last timed step (per view) for the byte model
-    for s in range(B):
-        l, r = eng.cells(s)
-        cells += l + r
-    t = torch.tensor([ms], dtype=torch.float64, device=device)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    # searched cells summed over the timed steps (all sequences, both views),
+    # averaged per step for the byte model
+    _lib.call("es_ctx_cells_acc", eng._h, ctypes.byref(acc), 1)
+    cells = acc.value / K
+    ms_max = sharding.max_over_ranks(ms, device)
     frames_total = B * K * world
     value = frames_total / (ms_max / 1e3)
 
@@ -268,8 +266,7 @@ def main():
             bp.process_frames(host.numpy(), motions_for(specs, k), sync=True)
         staged = [imgs[Wm + i].cpu().pin_memory() for i in range(K)]
         outs = [torch.empty((B, H, W), dtype=torch.int16, pin_memory=True) for _ in range(K)]
-        if world > 1:
-            dist.barrier()
+        sharding.barrier()
         torch.cuda.synchronize(device)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(ext):
@@ -283,10 +280,8 @@ def main():
             e1.record()
         bp.sync()
         torch.cuda.synchronize(device)
-        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": frames_total / (float(te.item()) / 1e3), "unit": "frames/s",
+        te = sharding.max_over_ranks(e0.elapsed_time(e1), device)
+        e2e = {"value": frames_total / (te / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": int(B * 2 * H * W), "d2h_bytes_per_step": int(B * H * W * 2)}
 
     # ---- roofline of the dominant kernel (aggregation stage) ------------

@@ -78,6 +78,9 @@ int es_ctx_sync(es_ctx* ctx);
 /* frame counter of sequence s (FilterState.frame) and searched cells per view */
 int es_ctx_frame(es_ctx* ctx, int seq, int64_t* frame);
 int es_ctx_cells(es_ctx* ctx, int seq, uint64_t* cells_left, uint64_t* cells_right);
+/* searched cells summed over all sequences, views and steps since the last
+ * reset (syncs the context stream) */
+int es_ctx_cells_acc(es_ctx* ctx, uint64_t* total, int reset);
 /* pipeline.py:122 have_state of sequence s after the last synced step */
 int es_ctx_have_state(es_ctx* ctx, int seq, int64_t* have);
 /* per-stage CUDA-event timing on the context's stream: when enabled every

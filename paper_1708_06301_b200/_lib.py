@@ -60,6 +60,7 @@ SIGNATURES = {
     "es_ctx_frame": [_P, _I, _P],
     "es_ctx_cells": [_P, _I, _P, _P],
     "es_ctx_have_state": [_P, _I, _P],
+    "es_ctx_cells_acc": [_P, _P, _I],
     "es_ctx_profile": [_P, _I],
     "es_ctx_stage_times": [_P, _P, _P],
     "es_ctx_export": [_P, _I, _I, _I, _P],

@@ -190,6 +190,7 @@ struct es_ctx {
   bool profiling = false;
   std::vector<std::array<cudaEvent_t, NSTAGE + 1>> prof;
   uint16_t* kitti = nullptr;   // batched KITTI export staging
+  unsigned long long* cells_acc = nullptr;   // searched cells summed over steps
   int lanes = 0;               // SGM lanes per chain (0 = heuristic)
   double last_fraction = 1.0;  // search fraction of the last synced step
 
@@ -208,7 +209,7 @@ int ctx_free(es_ctx* c) {
   void* ptrs[] = {c->img, c->sd[0], c->sd[1], c->sp[0], c->sp[1], c->sv[0], c->sv[1], c->hd,
                   c->hp, c->hv, c->pd, c->pp, c->pv, c->zkey, c->zidx, c->meta, c->C, c->S,
                   c->dstar, c->r, c->mvalid, c->keep, c->Hm, c->have_pred, c->err, c->anyv,
-                  c->cells, c->kitti};
+                  c->cells, c->kitti, c->cells_acc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   void* hptrs[] = {c->h_Hm, c->h_have, c->h_err, c->h_anyv, c->h_cells};
@@ -243,6 +244,7 @@ PredArgs pred_args(es_ctx* c) {
   a.meta = c->meta;
   a.cells = c->cells;
   a.err = c->err;
+  a.cells_acc = c->cells_acc;
   return a;
 }
 
@@ -311,6 +313,9 @@ int es_ctx_create(int device, const es_rig* rig, const es_params* prm, int batch
   if (!e) e = dalloc(&c->err, batch);
   if (!e) e = dalloc(&c->anyv, batch);
   if (!e) e = dalloc(&c->cells, 2 * (size_t)batch);
+  if (!e) e = dalloc(&c->cells_acc, 1);
+  if (!e && cudaMemset(c->cells_acc, 0, sizeof(unsigned long long)) != cudaSuccess)
+    e = fail(ES_ERR_CUDA, "cudaMemset failed");
   if (e) {
     ctx_free(c);
     return e;
@@ -521,6 +526,16 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
 int es_ctx_frame(es_ctx* c, int seq, int64_t* frame) {
   if (seq < 0 || seq >= c->B) return fail(ES_ERR_VALUE, "sequence index out of range");
   *frame = c->frame[seq];
+  return ES_OK;
+}
+
+int es_ctx_cells_acc(es_ctx* c, uint64_t* total, int reset) {
+  CK(cudaSetDevice(c->device));
+  unsigned long long v = 0;
+  CK(cudaMemcpyAsync(&v, c->cells_acc, sizeof(v), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  *total = v;
+  if (reset) CK(cudaMemsetAsync(c->cells_acc, 0, sizeof(v), c->st));
   return ES_OK;
 }
 

@@ -27,6 +27,7 @@ struct PredArgs {
   uint2* meta;               // lo | hi << 16, pair offset
   unsigned long long* cells; // [n_sv] searched cells (sum of widths)
   int* err;                  // [n_seq] error bits
+  unsigned long long* cells_acc = nullptr;  // optional running total over steps
 };
 
 void launch_predict(const PredArgs& a, int n_sv, cudaStream_t st);

@@ -211,7 +211,10 @@ __global__ void __launch_bounds__(NT) k_fill_v_intervals(PredArgs a) {
   }
   atomicAdd(&cells_smem, my_cells);
   __syncthreads();
-  if (threadIdx.x == 0) atomicAdd(a.cells + sv, cells_smem);
+  if (threadIdx.x == 0) {
+    atomicAdd(a.cells + sv, cells_smem);
+    if (a.cells_acc) atomicAdd(a.cells_acc, cells_smem);
+  }
 }
 
 // meta from caller-supplied intervals (stage-level matching_cost / variance)

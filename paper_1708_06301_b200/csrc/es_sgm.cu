@@ -404,6 +404,194 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp(SgmArgs a, int fam, 
   }
 }
 
+// ------------------------------------------------------------ v4 (u16)
+//
+// Same lane mapping as k_sgm_grp, but the predecessor's path values live in
+// shared memory (absolute pair index, double-buffered), so a step loops
+// dynamically over just the union of its chains' chunks, and the next
+// step's cost / partial-sum pairs are staged into shared memory with
+// cp.async while the current step computes.
+
+constexpr int V4_WARPS = 8;
+
+__device__ __forceinline__ void cp_async4(uint32_t* smem_dst, const uint32_t* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait1() {
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+}
+
+template <int G>
+__global__ void __launch_bounds__(V4_WARPS * 32) k_sgm_v4(SgmArgs a, int fam, int sweeps,
+                                                           int init) {
+  constexpr int NG = 32 / G;
+  constexpr uint32_t NONE = 0xFFFFFFFFu;
+  extern __shared__ uint32_t v4smem[];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int gl = lane & (G - 1);
+  const int grp = lane / G;
+  const int gbase = lane & ~(G - 1);
+  const int W = a.W, H = a.H;
+  const int NP = npairs_max(a.d_max);
+  const int NPP = NP + 2;
+  const int nchains = fam == FAM_H ? H : (fam == FAM_V ? W : W + H - 1);
+  const int c0 = (blockIdx.x * V4_WARPS + wid) * NG;
+  if (c0 >= nchains) return;
+  if (a.select) {
+    const double frac = (double)a.cells[blockIdx.y] / ((double)W * H * (a.d_max + 1));
+    if ((a.select == 1) == (frac > a.split)) return;
+  }
+  // per-warp shared memory: pbuf[2][NG][NPP], cst[2][NG][NP], sst[2][NG][NP]
+  uint32_t* wsm = v4smem + (size_t)wid * (2 * NG * NPP + 4 * NG * NP);
+  uint32_t* pbuf = wsm;
+  uint32_t* cst = wsm + 2 * NG * NPP;
+  uint32_t* sst = cst + 2 * NG * NP;
+  const int ch = c0 + grp;
+  const size_t HW = (size_t)W * H;
+  const uint2* __restrict__ meta = a.meta + (size_t)blockIdx.y * HW;
+  const uint32_t* __restrict__ C =
+      reinterpret_cast<const uint32_t*>(a.C) + (size_t)blockIdx.y * a.volcap;
+  uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
+  asm volatile("" : "+l"(C));
+  asm volatile("" : "+l"(S));
+  const uint32_t p1x2 = a.p1i * 0x10001u;
+  const uint32_t p2 = a.p2i;
+  const int len = fam == FAM_H ? W : H;
+  bool first_sweep = true;
+  for (int bwd = 0; bwd < 2; ++bwd) {
+    if (!(sweeps & (1 << bwd))) continue;
+    const bool init_sum = init && first_sweep;
+    first_sweep = false;
+    auto load_meta = [&](int tb) -> uint2 {
+      int x, y;
+      const int t = tb + gl;
+      if (t < len && grp_pixel(fam, bwd, ch, t, W, H, x, y)) return meta[(size_t)y * W + x];
+      return make_uint2(NONE, 0u);
+    };
+    // stage the operands of one step: group lanes copy its pairs
+    auto stage = [&](int slot, uint32_t my_, int span_) {
+      uint32_t* cd = cst + (slot * NG + grp) * NP;
+      uint32_t* sd = sst + (slot * NG + grp) * NP;
+      const int rounds = __reduce_max_sync(FULL, (span_ + G - 1) / G);
+      for (int k = 0; k < rounds; ++k) {
+        const int i = k * G + gl;
+        if (i < span_) {
+          cp_async4(cd + i, C + (my_ + (uint32_t)i));
+          if (!init_sum) cp_async4(sd + i, S + (my_ + (uint32_t)i));
+        }
+      }
+      cp_async_commit();
+    };
+    uint2 mb_cur = load_meta(0);
+    uint2 mb_next = load_meta(G);
+    int tb = 0;
+    const uint32_t mx0 = __shfl_sync(FULL, mb_cur.x, gbase);
+    uint32_t my = __shfl_sync(FULL, mb_cur.y, gbase);
+    int j0 = 0, j1 = -1;
+    if (mx0 != NONE) {
+      j0 = (int)((mx0 & 0xFFFFu) >> 1);
+      j1 = (int)((mx0 >> 16) >> 1);
+    }
+    int jp0 = 0, jp1 = -1;   // predecessor's pair range (empty: no predecessor)
+    stage(0, my, j1 - j0 + 1);
+    uint32_t m = 0;
+    int rp = 0;
+    for (int t = 0; t < len; ++t) {
+      // ---- next step: meta, stage its operands
+      int j0n = 0, j1n = -1;
+      uint32_t my1 = 0;
+      if (t + 1 < len) {
+        if (t + 1 == tb + G) {
+          tb += G;
+          mb_cur = mb_next;
+          mb_next = load_meta(tb + G);
+        }
+        const int r = t + 1 - tb;
+        const uint32_t mx1 = __shfl_sync(FULL, mb_cur.x, gbase | r);
+        my1 = __shfl_sync(FULL, mb_cur.y, gbase | r);
+        if (mx1 != NONE) {
+          j0n = (int)((mx1 & 0xFFFFu) >> 1);
+          j1n = (int)((mx1 >> 16) >> 1);
+        }
+      }
+      stage((t + 1) & 1, my1, j1n - j0n + 1);
+      cp_async_wait1();   // this step's staged operands have landed
+      __syncwarp();
+      // ---- this step over the union of the chains' chunks
+      const bool act = j1 >= j0;
+      const bool first = act && jp1 < jp0;
+      const int ulo = __reduce_min_sync(FULL, act ? j0 / G : 0x7fff);
+      const int uhi = __reduce_max_sync(FULL, act ? j1 / G : -1);
+      const uint32_t mp2 = (m + p2) * 0x10001u;
+      const uint32_t ng = ((0x10000u - m) & 0xFFFFu) * 0x10001u;
+      const uint32_t* pr_ = pbuf + (rp * NG + grp) * NPP + 1;        // predecessor
+      uint32_t* pw_ = pbuf + ((rp ^ 1) * NG + grp) * NPP + 1;        // this pixel
+      const uint32_t* cs = cst + ((t & 1) * NG + grp) * NP;
+      const uint32_t* ss = sst + ((t & 1) * NG + grp) * NP;
+      const uint32_t pspan = (uint32_t)(jp1 - jp0 + 1);
+      const uint32_t span = (uint32_t)(j1 - j0 + 1);
+      uint32_t nmin = INF16x2;
+      for (int c = ulo; c <= uhi; ++c) {
+        const int j = c * G + gl;
+        const uint32_t rel = (uint32_t)(j - j0);
+        const bool in = rel < span;
+        if (in) {
+          const uint32_t cv = cs[rel];
+          uint32_t L;
+          if (first) {
+            L = cv;
+          } else {
+            const uint32_t pv = (uint32_t)(j - jp0) < pspan ? pr_[j] : INF16x2;
+            const uint32_t pl = (uint32_t)(j - 1 - jp0) < pspan ? pr_[j - 1] : INF16x2;
+            const uint32_t pr = (uint32_t)(j + 1 - jp0) < pspan ? pr_[j + 1] : INF16x2;
+            const uint32_t nb =
+                __vminu2(__byte_perm(pl, pv, 0x5432), __byte_perm(pv, pr, 0x5432));
+            const uint32_t cand = __vminu2(__viaddmin_u16x2(nb, p1x2, pv), mp2);
+            L = __vadd2(cv, __vadd2(cand, ng));
+          }
+          pw_[j] = L;
+          nmin = __vminu2(nmin, L);
+          S[my + rel] = init_sum ? L : __vadd2(ss[rel], L);
+        }
+      }
+      const uint32_t hm = min(nmin & 0xFFFFu, nmin >> 16);
+      uint32_t mg = 0;
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const uint32_t r = __reduce_min_sync(FULL, grp == g ? hm : 0xFFFFFFFFu);
+        if (grp == g) mg = r;
+      }
+      __syncwarp();   // this step's pbuf writes / stage reads before reuse
+      m = mg;
+      jp0 = j0;
+      jp1 = j1;
+      j0 = j0n;
+      j1 = j1n;
+      my = my1;
+      rp ^= 1;
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncwarp();
+  }
+}
+
+template <int G>
+static void launch_v4(const SgmArgs& a, int fam, int sweeps, int init, int n_sv, cudaStream_t st) {
+  const int nchains = fam == FAM_H ? a.H : (fam == FAM_V ? a.W : a.W + a.H - 1);
+  constexpr int NG = 32 / G;
+  constexpr int per_block = V4_WARPS * NG;
+  const int NP = npairs_max(a.d_max);
+  const size_t smem = sizeof(uint32_t) * V4_WARPS * (2 * NG * (NP + 2) + 4 * NG * NP);
+  dim3 grid((nchains + per_block - 1) / per_block, n_sv);
+  cudaFuncSetAttribute(k_sgm_v4<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_sgm_v4<G><<<grid, V4_WARPS * 32, smem, st>>>(a, fam, sweeps, init);
+}
+
 template <int G>
 static void launch_grp(const SgmArgs& a, int nch_pairs, int fam, int sweeps, int init, int n_sv,
                        cudaStream_t st) {
@@ -421,7 +609,26 @@ static void launch_grp(const SgmArgs& a, int nch_pairs, int fam, int sweeps, int
 static void launch_family_seg(const SgmArgs& a, int fam, int sweeps, int init, int n_sv,
                               cudaStream_t st) {
   static const int forced = getenv("ES_SGM_G") ? atoi(getenv("ES_SGM_G")) : 0;
+  static const bool use_v3 = getenv("ES_SGM_V3") != nullptr;   // A/B switch
   const int np = npairs_max(a.d_max);
+  if (!use_v3) {
+    if (!forced && !a.lanes && a.cells) {
+      // measured: reduced intervals run best in the shared-memory
+      // v4 kernel with 8 lanes per chain, wide ones in the register kernel
+      // with 16 lanes per chain
+      SgmArgs lo = a, hi = a;
+      lo.select = 1;
+      hi.select = 2;
+      launch_v4<8>(lo, fam, sweeps, init, n_sv, st);
+      launch_grp<16>(hi, np, fam, sweeps, init, n_sv, st);
+      return;
+    }
+    const int g = forced ? forced : (a.lanes ? a.lanes : 8);
+    if (g >= 32) launch_v4<32>(a, fam, sweeps, init, n_sv, st);
+    else if (g >= 16) launch_v4<16>(a, fam, sweeps, init, n_sv, st);
+    else launch_v4<8>(a, fam, sweeps, init, n_sv, st);
+    return;
+  }
   if (!forced && !a.lanes && a.cells) {
     SgmArgs lo = a, hi = a;
     lo.select = 1;

@@ -1,0 +1,56 @@
+"""World-size-2 gloo run of the sharded benchmark's host logic on CPU:
+disjoint sequence shards, barrier, max-over-ranks timing, rank-0 report."""
+
+import os
+import socket
+
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1708_06301_b200 import sharding
+    r, w, local = sharding.world()
+    seeds = sharding.rank_sequences(r, w, per_rank=4)
+    sharding.barrier()
+    elapsed = 10.0 + 5.0 * r          # rank 1 is slower
+    ms = sharding.max_over_ranks(elapsed)
+    gathered = [None] * w
+    dist.all_gather_object(gathered, seeds)
+    out[rank] = (seeds, ms, gathered, local)
+    dist.destroy_process_group()
+
+
+def test_two_rank_sharding_and_timing():
+    world = 2
+    port = _free_port()
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    s0, ms0, all0, l0 = res[0]
+    s1, ms1, all1, l1 = res[1]
+    assert set(s0).isdisjoint(s1) and len(s0) == len(s1) == 4
+    assert ms0 == ms1 == 15.0                 # max over ranks, identical everywhere
+    assert all0 == all1 == [s0, s1]
+    assert (l0, l1) == (0, 1)
+
+
+def test_single_process_is_identity():
+    from paper_1708_06301_b200 import sharding
+    assert sharding.max_over_ranks(3.5) == 3.5
+    assert sharding.rank_sequences(0, 1, 3, seed0=7) == [7, 8, 9]
+    with pytest.raises(ValueError):
+        sharding.rank_sequences(2, 2, 3)

@@ -404,6 +404,364 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp(SgmArgs a, int fam, 
   }
 }
 
+// ------------------------------------------------------------ grouped, depth 2
+//
+// k_sgm_grp with the operands fetched two steps ahead: two register sets
+// alternate (the step loop is unrolled by two so both stay statically
+// indexed), giving each load about two steps of compute to land.
+
+struct GrpStep {          // per-step scalars of one chain (uniform in its group)
+  uint32_t my;            // pair offset of the pixel
+  int j0;                 // first pair
+  uint32_t span;          // number of pairs (0: no pixel)
+  uint32_t um;            // warp-uniform chunk mask (union over the warp's chains)
+};
+
+template <int G, int NCH, int PF>
+__global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp2(SgmArgs a, int fam, int sweeps,
+                                                              int init) {
+  constexpr int NG = 32 / G;
+  constexpr uint32_t NONE = 0xFFFFFFFFu;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int grp = lane / G;
+  const int gbase = lane & ~(G - 1);
+  const int W = a.W, H = a.H;
+  const int nchains = fam == FAM_H ? H : (fam == FAM_V ? W : W + H - 1);
+  const int c0 = (blockIdx.x * GRP_WARPS + (threadIdx.x >> 5)) * NG;
+  if (c0 >= nchains) return;
+  if (a.select) {
+    const double frac = (double)a.cells[blockIdx.y] / ((double)W * H * (a.d_max + 1));
+    if ((a.select == 1) == (frac > a.split)) return;
+  }
+  const int ch = c0 + grp;
+  const size_t HW = (size_t)W * H;
+  const uint2* __restrict__ meta = a.meta + (size_t)blockIdx.y * HW;
+  const uint32_t* __restrict__ C =
+      reinterpret_cast<const uint32_t*>(a.C) + (size_t)blockIdx.y * a.volcap;
+  uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
+  asm volatile("" : "+l"(C));
+  asm volatile("" : "+l"(S));
+  const uint32_t p1x2 = a.p1i * 0x10001u;
+  const uint32_t p2 = a.p2i;
+  const int len = fam == FAM_H ? W : H;
+  const int src_l = gbase | ((gl + G - 1) & (G - 1));
+  const int src_r = gbase | ((gl + 1) & (G - 1));
+  auto umask = [](int lo, int hi) -> uint32_t {
+    return hi < lo ? 0u : ((hi >= 31 ? 0xFFFFFFFFu : ((2u << hi) - 1u)) & ~((1u << lo) - 1u));
+  };
+  bool first_sweep = true;
+  for (int bwd = 0; bwd < 2; ++bwd) {
+    if (!(sweeps & (1 << bwd))) continue;
+    const bool init_sum = init && first_sweep;
+    first_sweep = false;
+    auto load_meta = [&](int tb) -> uint2 {
+      int x, y;
+      const int t = tb + gl;
+      if (t < len && grp_pixel(fam, bwd, ch, t, W, H, x, y)) return meta[(size_t)y * W + x];
+      return make_uint2(NONE, 0u);
+    };
+    uint2 mb_cur = load_meta(0);
+    uint2 mb_next = load_meta(G);
+    int tb = 0;
+    // scalars of step t' (t' < len), from the two meta batches
+    auto info = [&](int tp) -> GrpStep {
+      GrpStep s{0u, 0, 0u, 0u};
+      int clo = NCH, chi = -1;
+      if (tp < len) {
+        if (tp == tb + G) {   // rotate the batches; the new one is used G steps later
+          tb += G;
+          mb_cur = mb_next;
+          mb_next = load_meta(tb + G);
+        }
+        const int r = tp - tb;
+        const uint32_t mx = __shfl_sync(FULL, mb_cur.x, gbase | r);
+        s.my = __shfl_sync(FULL, mb_cur.y, gbase | r);
+        if (mx != NONE) {
+          s.j0 = (int)((mx & 0xFFFFu) >> 1);
+          const int j1 = (int)((mx >> 16) >> 1);
+          s.span = (uint32_t)(j1 - s.j0 + 1);
+          clo = s.j0 / G;
+          chi = j1 / G;
+        }
+      }
+      s.um = umask(__reduce_min_sync(FULL, clo), __reduce_max_sync(FULL, chi));
+      return s;
+    };
+    auto fetch = [&](const GrpStep& s, uint32_t (&cn)[NCH], uint32_t (&sn)[NCH], int c) {
+      const uint32_t rel = (uint32_t)(c * G + gl - s.j0);
+      const bool in = rel < s.span;
+      cn[c] = in ? __ldg(C + (s.my + rel)) : INF16x2;
+      sn[c] = (in && !init_sum) ? S[s.my + rel] : 0u;
+    };
+    uint32_t prev[NCH], cs[PF][NCH], ss[PF][NCH];
+    GrpStep sq[PF];
+#pragma unroll
+    for (int p = 0; p < PF; ++p) sq[p] = info(p);
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      prev[c] = INF16x2;
+#pragma unroll
+      for (int p = 0; p < PF; ++p) fetch(sq[p], cs[p], ss[p], c);
+    }
+    uint32_t m = 0;
+    bool was_active = false;
+    // one step: consume (cn, sn) for step t (scalars cur), refill them with
+    // step t+2 (scalars nn)
+    auto step = [&](const GrpStep& cur, const GrpStep& nn, uint32_t (&cn)[NCH],
+                    uint32_t (&sn)[NCH]) {
+      const bool act = cur.span != 0;
+      const bool first = act && !was_active;
+      const uint32_t mp2 = (m + p2) * 0x10001u;
+      const uint32_t ng = ((0x10000u - m) & 0xFFFFu) * 0x10001u;
+      uint32_t nmin = INF16x2;
+      uint32_t left_old = INF16x2;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const uint32_t pv = prev[c];
+        if ((cur.um >> c) & 1u) {
+          const uint32_t srcl = gl == G - 1 ? left_old : pv;
+          const uint32_t srcr =
+              gl == 0 ? (c + 1 < NCH ? prev[c + 1 < NCH ? c + 1 : c] : INF16x2) : pv;
+          const uint32_t pl = __shfl_sync(FULL, srcl, src_l);
+          const uint32_t pr = __shfl_sync(FULL, srcr, src_r);
+          const uint32_t nb = __vminu2(__byte_perm(pl, pv, 0x5432), __byte_perm(pv, pr, 0x5432));
+          const uint32_t cand = __vminu2(__viaddmin_u16x2(nb, p1x2, pv), mp2);
+          const uint32_t L = first ? cn[c] : __vadd2(cn[c], __vadd2(cand, ng));
+          prev[c] = L;
+          nmin = __vminu2(nmin, L);
+          const uint32_t rel = (uint32_t)(c * G + gl - cur.j0);
+          if (rel < cur.span) S[cur.my + rel] = init_sum ? L : __vadd2(sn[c], L);
+        } else {
+          prev[c] = INF16x2;
+        }
+        left_old = pv;
+        if ((nn.um >> c) & 1u) fetch(nn, cn, sn, c);
+      }
+      const uint32_t hm = min(nmin & 0xFFFFu, nmin >> 16);
+      uint32_t mg = 0;
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const uint32_t r = __reduce_min_sync(FULL, grp == g ? hm : 0xFFFFFFFFu);
+        if (grp == g) mg = r;
+      }
+      m = mg;
+      was_active = act;
+    };
+    for (int t = 0; t < len; t += PF) {
+#pragma unroll
+      for (int p = 0; p < PF; ++p) {
+        if (t + p < len) {
+          const GrpStep nx = info(t + p + PF);
+          step(sq[p], nx, cs[p], ss[p]);
+          sq[p] = nx;
+        }
+      }
+    }
+  }
+}
+
+template <int G>
+static void launch_grp2(const SgmArgs& a, int nch_pairs, int fam, int sweeps, int init, int n_sv,
+                        cudaStream_t st) {
+  const int nchains = fam == FAM_H ? a.H : (fam == FAM_V ? a.W : a.W + a.H - 1);
+  constexpr int per_block = GRP_WARPS * (32 / G);
+  dim3 grid((nchains + per_block - 1) / per_block, n_sv);
+  const int nch = (nch_pairs + G - 1) / G;
+  static const int pf = getenv("ES_SGM_PF") ? atoi(getenv("ES_SGM_PF")) : 3;
+  auto go = [&](auto kern) { kern<<<grid, GRP_WARPS * 32, 0, st>>>(a, fam, sweeps, init); };
+  if (nch <= 4) {
+    if (pf <= 2) go(k_sgm_grp2<G, 4, 2>);
+    else if (pf == 3) go(k_sgm_grp2<G, 4, 3>);
+    else go(k_sgm_grp2<G, 4, 4>);
+  } else if (nch <= 8) {
+    if (pf <= 2) go(k_sgm_grp2<G, 8, 2>);
+    else if (pf == 3) go(k_sgm_grp2<G, 8, 3>);
+    else go(k_sgm_grp2<G, 8, 4>);
+  } else if (nch <= 16) {
+    go(k_sgm_grp2<G, 16, 2>);
+  } else {
+    go(k_sgm_grp2<G, 32, 2>);
+  }
+}
+
+// ------------------------------------------------------------ grouped, 2 pairs/lane
+//
+// As k_sgm_grp2 (two-step-ahead operand prefetch) but every lane owns two
+// consecutive pairs (4 cells): lane g of chunk c holds pairs
+// c*2G + 2g and c*2G + 2g + 1.  The shuffles, selects, chunk-mask tests and
+// address arithmetic are shared by four cells, and the byte permute that
+// forms "right neighbours of the first pair" is also "left neighbours of the
+// second pair".
+
+template <int G, int NCH>
+__global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp3(SgmArgs a, int fam, int sweeps,
+                                                              int init) {
+  constexpr int NG = 32 / G;
+  constexpr int CW = 2 * G;   // pairs per chunk
+  constexpr uint32_t NONE = 0xFFFFFFFFu;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int grp = lane / G;
+  const int gbase = lane & ~(G - 1);
+  const int W = a.W, H = a.H;
+  const int nchains = fam == FAM_H ? H : (fam == FAM_V ? W : W + H - 1);
+  const int c0 = (blockIdx.x * GRP_WARPS + (threadIdx.x >> 5)) * NG;
+  if (c0 >= nchains) return;
+  if (a.select) {
+    const double frac = (double)a.cells[blockIdx.y] / ((double)W * H * (a.d_max + 1));
+    if ((a.select == 1) == (frac > a.split)) return;
+  }
+  const int ch = c0 + grp;
+  const size_t HW = (size_t)W * H;
+  const uint2* __restrict__ meta = a.meta + (size_t)blockIdx.y * HW;
+  const uint32_t* __restrict__ C =
+      reinterpret_cast<const uint32_t*>(a.C) + (size_t)blockIdx.y * a.volcap;
+  uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
+  asm volatile("" : "+l"(C));
+  asm volatile("" : "+l"(S));
+  const uint32_t p1x2 = a.p1i * 0x10001u;
+  const uint32_t p2 = a.p2i;
+  const int len = fam == FAM_H ? W : H;
+  const int src_l = gbase | ((gl + G - 1) & (G - 1));
+  const int src_r = gbase | ((gl + 1) & (G - 1));
+  auto umask = [](int lo, int hi) -> uint32_t {
+    return hi < lo ? 0u : ((hi >= 31 ? 0xFFFFFFFFu : ((2u << hi) - 1u)) & ~((1u << lo) - 1u));
+  };
+  bool first_sweep = true;
+  for (int bwd = 0; bwd < 2; ++bwd) {
+    if (!(sweeps & (1 << bwd))) continue;
+    const bool init_sum = init && first_sweep;
+    first_sweep = false;
+    auto load_meta = [&](int tb) -> uint2 {
+      int x, y;
+      const int t = tb + gl;
+      if (t < len && grp_pixel(fam, bwd, ch, t, W, H, x, y)) return meta[(size_t)y * W + x];
+      return make_uint2(NONE, 0u);
+    };
+    uint2 mb_cur = load_meta(0);
+    uint2 mb_next = load_meta(G);
+    int tb = 0;
+    auto info = [&](int tp) -> GrpStep {
+      GrpStep s{0u, 0, 0u, 0u};
+      int clo = NCH, chi = -1;
+      if (tp < len) {
+        if (tp == tb + G) {
+          tb += G;
+          mb_cur = mb_next;
+          mb_next = load_meta(tb + G);
+        }
+        const int r = tp - tb;
+        const uint32_t mx = __shfl_sync(FULL, mb_cur.x, gbase | r);
+        s.my = __shfl_sync(FULL, mb_cur.y, gbase | r);
+        if (mx != NONE) {
+          s.j0 = (int)((mx & 0xFFFFu) >> 1);
+          const int j1 = (int)((mx >> 16) >> 1);
+          s.span = (uint32_t)(j1 - s.j0 + 1);
+          clo = s.j0 / CW;
+          chi = j1 / CW;
+        }
+      }
+      s.um = umask(__reduce_min_sync(FULL, clo), __reduce_max_sync(FULL, chi));
+      return s;
+    };
+    // operands of chunk c for one step: two pairs per lane
+    auto fetch = [&](const GrpStep& s, uint32_t (&cn)[2 * NCH], uint32_t (&sn)[2 * NCH], int c) {
+      const uint32_t rel = (uint32_t)(c * CW + 2 * gl - s.j0);
+      const bool in0 = rel < s.span, in1 = rel + 1 < s.span;
+      cn[2 * c] = in0 ? __ldg(C + (s.my + rel)) : INF16x2;
+      cn[2 * c + 1] = in1 ? __ldg(C + (s.my + rel + 1)) : INF16x2;
+      sn[2 * c] = (in0 && !init_sum) ? S[s.my + rel] : 0u;
+      sn[2 * c + 1] = (in1 && !init_sum) ? S[s.my + rel + 1] : 0u;
+    };
+    uint32_t prev[2 * NCH], cA[2 * NCH], sA[2 * NCH], cB[2 * NCH], sB[2 * NCH];
+    GrpStep s0 = info(0);
+    GrpStep s1 = info(1);
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      prev[2 * c] = INF16x2;
+      prev[2 * c + 1] = INF16x2;
+      fetch(s0, cA, sA, c);
+      fetch(s1, cB, sB, c);
+    }
+    uint32_t m = 0;
+    bool was_active = false;
+    auto step = [&](const GrpStep& cur, const GrpStep& nn, uint32_t (&cn)[2 * NCH],
+                    uint32_t (&sn)[2 * NCH]) {
+      const bool act = cur.span != 0;
+      const bool first = act && !was_active;
+      const uint32_t mp2 = (m + p2) * 0x10001u;
+      const uint32_t ng = ((0x10000u - m) & 0xFFFFu) * 0x10001u;
+      uint32_t nmin = INF16x2;
+      uint32_t left_old = INF16x2;   // previous chunk's second pair, before overwrite
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const uint32_t pa = prev[2 * c], pb = prev[2 * c + 1];
+        if ((cur.um >> c) & 1u) {
+          // left neighbour of pair a: the previous lane's pair b (or the
+          // previous chunk's last one); right neighbour of pair b: the next
+          // lane's pair a (or the next chunk's first one)
+          const uint32_t srcl = gl == G - 1 ? left_old : pb;
+          const uint32_t srcr =
+              gl == 0 ? (c + 1 < NCH ? prev[c + 1 < NCH ? 2 * c + 2 : 0] : INF16x2) : pa;
+          const uint32_t pl = __shfl_sync(FULL, srcl, src_l);
+          const uint32_t pr = __shfl_sync(FULL, srcr, src_r);
+          const uint32_t mid = __byte_perm(pa, pb, 0x5432);
+          const uint32_t nba = __vminu2(__byte_perm(pl, pa, 0x5432), mid);
+          const uint32_t nbb = __vminu2(mid, __byte_perm(pb, pr, 0x5432));
+          const uint32_t ca = __vminu2(__viaddmin_u16x2(nba, p1x2, pa), mp2);
+          const uint32_t cb = __vminu2(__viaddmin_u16x2(nbb, p1x2, pb), mp2);
+          const uint32_t La = first ? cn[2 * c] : __vadd2(cn[2 * c], __vadd2(ca, ng));
+          const uint32_t Lb = first ? cn[2 * c + 1] : __vadd2(cn[2 * c + 1], __vadd2(cb, ng));
+          prev[2 * c] = La;
+          prev[2 * c + 1] = Lb;
+          nmin = __vminu2(nmin, __vminu2(La, Lb));
+          const uint32_t rel = (uint32_t)(c * CW + 2 * gl - cur.j0);
+          if (rel < cur.span) S[cur.my + rel] = init_sum ? La : __vadd2(sn[2 * c], La);
+          if (rel + 1 < cur.span) S[cur.my + rel + 1] = init_sum ? Lb : __vadd2(sn[2 * c + 1], Lb);
+        } else {
+          prev[2 * c] = INF16x2;
+          prev[2 * c + 1] = INF16x2;
+        }
+        left_old = pb;
+        if ((nn.um >> c) & 1u) fetch(nn, cn, sn, c);
+      }
+      const uint32_t hm = min(nmin & 0xFFFFu, nmin >> 16);
+      uint32_t mg = 0;
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const uint32_t r = __reduce_min_sync(FULL, grp == g ? hm : 0xFFFFFFFFu);
+        if (grp == g) mg = r;
+      }
+      m = mg;
+      was_active = act;
+    };
+    for (int t = 0; t < len; t += 2) {
+      const GrpStep s2 = info(t + 2);
+      step(s0, s2, cA, sA);
+      if (t + 1 >= len) break;
+      const GrpStep s3 = info(t + 3);
+      step(s1, s3, cB, sB);
+      s0 = s2;
+      s1 = s3;
+    }
+  }
+}
+
+template <int G>
+static void launch_grp3(const SgmArgs& a, int nch_pairs, int fam, int sweeps, int init, int n_sv,
+                        cudaStream_t st) {
+  const int nchains = fam == FAM_H ? a.H : (fam == FAM_V ? a.W : a.W + a.H - 1);
+  constexpr int per_block = GRP_WARPS * (32 / G);
+  dim3 grid((nchains + per_block - 1) / per_block, n_sv);
+  const int nch = (nch_pairs + 2 * G - 1) / (2 * G);
+  auto go = [&](auto kern) { kern<<<grid, GRP_WARPS * 32, 0, st>>>(a, fam, sweeps, init); };
+  if (nch <= 2) go(k_sgm_grp3<G, 2>);
+  else if (nch <= 4) go(k_sgm_grp3<G, 4>);
+  else if (nch <= 8) go(k_sgm_grp3<G, 8>);
+  else go(k_sgm_grp3<G, 16>);
+}
+
 // ------------------------------------------------------------ v4 (u16)
 //
 // Same lane mapping as k_sgm_grp, but the predecessor's path values live in
@@ -619,8 +977,23 @@ static void launch_family_seg(const SgmArgs& a, int fam, int sweeps, int init, i
       SgmArgs lo = a, hi = a;
       lo.select = 1;
       hi.select = 2;
-      launch_v4<8>(lo, fam, sweeps, init, n_sv, st);
-      launch_grp<16>(hi, np, fam, sweeps, init, n_sv, st);
+      static const int variant = getenv("ES_SGM_VAR") ? atoi(getenv("ES_SGM_VAR")) : 0;
+      if (variant == 1) {          // one pair per lane, depth-2 prefetch
+        launch_grp2<8>(lo, np, fam, sweeps, init, n_sv, st);
+        launch_grp2<16>(hi, np, fam, sweeps, init, n_sv, st);
+      } else if (variant == 2) {   // shared-memory v4 for reduced intervals
+        launch_v4<8>(lo, fam, sweeps, init, n_sv, st);
+        launch_grp2<16>(hi, np, fam, sweeps, init, n_sv, st);
+      } else if (variant == 3) {   // two pairs per lane, 16 lanes for wide intervals
+        launch_v4<8>(lo, fam, sweeps, init, n_sv, st);
+        launch_grp3<16>(hi, np, fam, sweeps, init, n_sv, st);
+      } else if (variant == 4) {   // two pairs per lane everywhere
+        launch_grp3<4>(lo, np, fam, sweeps, init, n_sv, st);
+        launch_grp3<8>(hi, np, fam, sweeps, init, n_sv, st);
+      } else {                     // default: measured best per regime
+        launch_v4<8>(lo, fam, sweeps, init, n_sv, st);
+        launch_grp3<8>(hi, np, fam, sweeps, init, n_sv, st);
+      }
       return;
     }
     const int g = forced ? forced : (a.lanes ? a.lanes : 8);

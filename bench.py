@@ -43,7 +43,7 @@ H, W, D_MAX = 375, 1242, 127
 RIG = dict(f=718.9, b=0.54, cx=607.0, cy=185.0, width=W, height=H, d_max=D_MAX)
 SEQ_FRAMES = 50
 TEXTURE_SCALE = 0.05
-KERNELS_PER_STEP = 12   # zmax, zidx, fill_h, fill_v, cost, 4 x sgm, wta, fuse, any_valid
+KERNELS_PER_STEP = 15   # zmax, zidx, fill_h, fill_v, cost, 4 families x 2 sgm variants, wta, fuse
 
 
 def peaks():

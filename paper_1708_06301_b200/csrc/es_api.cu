@@ -150,6 +150,8 @@ struct es_ctx {
   int arith = ARITH_U16;
   size_t HW = 0, volcap = 0;
   cudaStream_t st = nullptr;
+  cudaStream_t st2 = nullptr;          // side stream for concurrent SGM variants
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   uint8_t* img = nullptr;
   double* sd[2] = {nullptr, nullptr};
   double* sp[2] = {nullptr, nullptr};
@@ -220,6 +222,9 @@ int ctx_free(es_ctx* c) {
   for (auto& a : c->prof)
     for (cudaEvent_t e : a) cudaEventDestroy(e);
   if (c->st) cudaStreamDestroy(c->st);
+  if (c->st2) cudaStreamDestroy(c->st2);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
   return ES_OK;
 }
@@ -329,7 +334,10 @@ int es_ctx_create(int device, const es_rig* rig, const es_params* prm, int batch
       cudaMallocHost(&c->h_err, sizeof(int) * batch) != cudaSuccess ||
       cudaMallocHost(&c->h_anyv, sizeof(int) * batch) != cudaSuccess ||
       cudaMallocHost(&c->h_cells, sizeof(unsigned long long) * 2 * batch) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     ctx_free(c);
     return fail(ES_ERR_CUDA, "pinned host / stream allocation failed");
   }
@@ -459,7 +467,16 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   // device from this frame's searched-cell count
   sa.lanes = c->lanes;
   sa.cells = c->cells;
-  launch_aggregate(sa, c->arith, n_sv, c->st);
+  if (c->arith == ARITH_U16 && !c->lanes && getenv("ES_SGM_VAR") == nullptr) {
+    // fork: wide-interval (seq, view)s run concurrently on the side stream
+    CK(cudaEventRecord(c->ev_fork, c->st));
+    CK(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
+    launch_aggregate_split(sa, n_sv, c->st, c->st2);
+    CK(cudaEventRecord(c->ev_join, c->st2));
+    CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
+  } else {
+    launch_aggregate(sa, c->arith, n_sv, c->st);
+  }
   mark(4);
 
   WtaArgs wa;
@@ -474,6 +491,8 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   wa.dstar = c->dstar;
   wa.r = c->r;
   wa.valid = c->mvalid;
+  wa.cells = c->cells;
+  wa.d_max = c->rig.d_max;
   launch_wta_variance(wa, n_sv, c->st);
   mark(5);
 
@@ -498,8 +517,8 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   fa.np_ = c->sp[nxt];
   fa.nv = c->sv[nxt];
   fa.keep = c->keep;
+  fa.any_valid = c->anyv;
   launch_checks_fuse(fa, B, c->st);
-  k_any_valid<<<dim3((unsigned)((HW + 255) / 256), n_sv), 256, 0, c->st>>>(c->sv[nxt], HW, c->anyv);
   mark(6);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(c->h_err, c->err, sizeof(int) * B, cudaMemcpyDeviceToHost, c->st));

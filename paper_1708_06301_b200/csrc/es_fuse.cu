@@ -36,31 +36,36 @@ __global__ void k_checks_fuse(FuseArgs a) {
   const int view = sv & 1;
   const size_t HW = (size_t)a.W * a.H;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int)HW) return;
-  const int x = i % a.W;
-  const size_t o = sv * HW + i;
-  const size_t po = (sv ^ 1) * HW + (i - x);   // partner view, same row
-  const int d = a.dstar[o];
-  const bool vm = a.mvalid[o] != 0;
-  bool keep = false;
-  if (vm) {
-    const int xo = view == 0 ? x - d : x + d;
-    if (xo >= 0 && xo < a.W && a.mvalid[po + xo] &&
-        fabs((double)d - (double)a.dstar[po + xo]) <= a.tau_lr) {
-      const uint2 mt = a.meta[o];
-      const uint32_t w = a.C[sv * a.volcap + mt.y + ((d >> 1) - (int)(lo_of(mt) >> 1))];
-      const uint32_t sad = (d & 1) ? (w >> 16) : (w & 0xFFFFu);
-      keep = (double)sad <= a.tau_sad;
+  bool nv = false;
+  if (i < (int)HW) {
+    const int x = i % a.W;
+    const size_t o = sv * HW + i;
+    const size_t po = (sv ^ 1) * HW + (i - x);   // partner view, same row
+    const int d = a.dstar[o];
+    const bool vm = a.mvalid[o] != 0;
+    bool keep = false;
+    if (vm) {
+      const int xo = view == 0 ? x - d : x + d;
+      if (xo >= 0 && xo < a.W && a.mvalid[po + xo] &&
+          fabs((double)d - (double)a.dstar[po + xo]) <= a.tau_lr) {
+        const uint2 mt = a.meta[o];
+        const uint32_t w = a.C[sv * a.volcap + mt.y + ((d >> 1) - (int)(lo_of(mt) >> 1))];
+        const uint32_t sad = (d & 1) ? (w >> 16) : (w & 0xFFFFu);
+        keep = (double)sad <= a.tau_sad;
+      }
     }
+    a.keep[o] = keep;
+    double nd, np;
+    kalman(a.pd[o], a.pp[o], a.pv[o] != 0, keep ? (double)d : 0.0, a.r[o], keep, a.p_init, nd,
+           np, nv);
+    a.nd[o] = nd;
+    a.np_[o] = np;
+    a.nv[o] = nv;
   }
-  a.keep[o] = keep;
-  double nd, np;
-  bool nv;
-  kalman(a.pd[o], a.pp[o], a.pv[o] != 0, keep ? (double)d : 0.0, a.r[o], keep, a.p_init, nd, np,
-         nv);
-  a.nd[o] = nd;
-  a.np_[o] = np;
-  a.nv[o] = nv;
+  // have_state of the next frame (pipeline.py:122): one flag per sequence,
+  // one atomic per block
+  if (__syncthreads_or(nv) && threadIdx.x == 0 && a.any_valid)
+    atomicOr(a.any_valid + (sv >> 1), 1);
 }
 
 void launch_checks_fuse(const FuseArgs& a, int n_seq, cudaStream_t st) {

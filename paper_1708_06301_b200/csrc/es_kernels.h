@@ -72,6 +72,8 @@ struct SgmArgs {
 // full 8-path aggregation; the u16 path runs 4 family launches (both sweeps
 // each), the f32 path runs the 8 directions in the reference's order
 void launch_aggregate(const SgmArgs& a, int arith, int n_sv, cudaStream_t st);
+// u16 only, a.cells required: reduced-interval (seq, view)s on st_lo, wide ones on st_hi
+void launch_aggregate_split(const SgmArgs& a, int n_sv, cudaStream_t st_lo, cudaStream_t st_hi);
 
 struct WtaArgs {
   int W, H;
@@ -84,6 +86,12 @@ struct WtaArgs {
   double* r;
   uint8_t* valid;
   const uint16_t* dstar_in = nullptr;  // optional caller winners (variance only)
+  // optional per-(seq, view) kernel choice as in SgmArgs: thread per pixel for
+  // reduced intervals, 8 lanes per pixel for wide ones
+  const unsigned long long* cells = nullptr;
+  int d_max = 0;
+  double split = 0.3;
+  int select = 0;
 };
 void launch_wta_variance(const WtaArgs& a, int n_sv, cudaStream_t st);
 
@@ -113,6 +121,7 @@ struct FuseArgs {
   double* np_;
   uint8_t* nv;
   uint8_t* keep;           // [n_sv]
+  int* any_valid = nullptr;  // [n_seq] set when the new state has a valid pixel
 };
 void launch_checks_fuse(const FuseArgs& a, int n_seq, cudaStream_t st);
 

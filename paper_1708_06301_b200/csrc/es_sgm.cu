@@ -1031,6 +1031,22 @@ static void launch_family(const SgmArgs& a, int nch, int fam, int sweeps, int in
   }
 }
 
+// u16 aggregation with the per-(seq, view) kernel choice: sequences with
+// reduced intervals run the v4 kernel on st_lo, wide ones the 2-pairs/lane
+// kernel on st_hi; each (seq, view) is handled by exactly one stream, so the
+// two streams never touch the same volume and run concurrently
+void launch_aggregate_split(const SgmArgs& a, int n_sv, cudaStream_t st_lo, cudaStream_t st_hi) {
+  SgmArgs lo = a, hi = a;
+  lo.select = 1;
+  hi.select = 2;
+  const int np = npairs_max(a.d_max);
+  const int fams[4] = {FAM_H, FAM_V, FAM_D1, FAM_D2};
+  for (int k = 0; k < 4; ++k) {
+    launch_v4<8>(lo, fams[k], 3, k == 0, n_sv, st_lo);
+    launch_grp3<8>(hi, np, fams[k], 3, k == 0, n_sv, st_hi);
+  }
+}
+
 void launch_aggregate(const SgmArgs& a, int arith, int n_sv, cudaStream_t st) {
   int nch = (npairs_max(a.d_max) + 31) / 32;
   if (nch > 4) nch = 8;
@@ -1139,34 +1155,9 @@ __global__ void __launch_bounds__(256) k_wta_var(WtaArgs a) {
 // 8-byte loads where aligned, then walks outward (sgm.py:319-344).  The
 // pairs of neighbouring pixels are adjacent, so a warp's loads stay within a
 // few cache lines and the walk re-reads from L1.
-__global__ void __launch_bounds__(256) k_wta_var_u16(WtaArgs a) {
-  const size_t HW = (size_t)a.W * a.H;
-  const size_t pix = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (pix >= HW) return;
-  const int svl = blockIdx.y;
-  const uint2 mt = a.meta[svl * HW + pix];
-  const int lo = lo_of(mt), hi = hi_of(mt);
-  const int j0 = lo >> 1, j1 = hi >> 1;
-  const uint32_t* s = reinterpret_cast<const uint32_t*>(a.S) + svl * a.volcap + mt.y;
-  // key = value << 16 | d: the minimum key is the smallest value, then d
-  uint32_t best = 0xFFFFFFFFu;
-  {
-    const uint32_t w = s[0];
-    const uint32_t d0 = 2u * j0;
-    if ((int)d0 >= lo) best = min(best, ((w & 0xFFFFu) << 16) | d0);
-    if ((int)d0 + 1 <= hi) best = min(best, (w & 0xFFFF0000u) | (d0 + 1));
-  }
-  for (int j = j0 + 1; j < j1; ++j) {
-    const uint32_t w = s[j - j0];
-    const uint32_t d0 = 2u * j;
-    best = min(best, min(((w & 0xFFFFu) << 16) | d0, (w & 0xFFFF0000u) | (d0 + 1)));
-  }
-  if (j1 > j0) {
-    const uint32_t w = s[j1 - j0];
-    const uint32_t d0 = 2u * j1;
-    best = min(best, ((w & 0xFFFFu) << 16) | d0);
-    if ((int)d0 + 1 <= hi) best = min(best, (w & 0xFFFF0000u) | (d0 + 1));
-  }
+// variance walk + outputs of one pixel given its argmin key (value<<16 | d)
+__device__ __forceinline__ void wta_finish(const WtaArgs& a, const uint32_t* s, int lo, int hi,
+                                           int j0, uint32_t best, size_t o) {
   const int dstar = (int)(best & 0xFFFFu);
   const uint32_t cstar = best >> 16;
   auto cell = [&](int d) -> uint32_t {
@@ -1186,16 +1177,99 @@ __global__ void __launch_bounds__(256) k_wta_var_u16(WtaArgs a) {
     if (!(acc < a.s_max)) break;
     ++count;
   }
-  const size_t o = svl * HW + pix;
   a.dstar[o] = (uint16_t)dstar;
   a.valid[o] = dstar > 0;
   a.r[o] = fmax((double)count, a.r_min);
 }
 
+__device__ __forceinline__ bool wta_skip(const WtaArgs& a, int svl) {
+  if (!a.select) return false;
+  const double frac = (double)a.cells[svl] / ((double)a.W * a.H * (a.d_max + 1));
+  return (a.select == 1) == (frac > a.split);
+}
+
+constexpr int WTA_GRID = 64;   // blocks per (seq, view), grid-stride: early exits stay cheap
+
+__global__ void __launch_bounds__(256) k_wta_var_u16(WtaArgs a) {
+  const size_t HW = (size_t)a.W * a.H;
+  const int svl = blockIdx.y;
+  if (wta_skip(a, svl)) return;
+  for (size_t pix = (size_t)blockIdx.x * blockDim.x + threadIdx.x; pix < HW;
+       pix += (size_t)gridDim.x * blockDim.x) {
+    const uint2 mt = a.meta[svl * HW + pix];
+    const int lo = lo_of(mt), hi = hi_of(mt);
+    const int j0 = lo >> 1, j1 = hi >> 1;
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(a.S) + svl * a.volcap + mt.y;
+    // key = value << 16 | d: the minimum key is the smallest value, then d
+    uint32_t best = 0xFFFFFFFFu;
+    {
+      const uint32_t w = s[0];
+      const uint32_t d0 = 2u * j0;
+      if ((int)d0 >= lo) best = min(best, ((w & 0xFFFFu) << 16) | d0);
+      if ((int)d0 + 1 <= hi) best = min(best, (w & 0xFFFF0000u) | (d0 + 1));
+    }
+    for (int j = j0 + 1; j < j1; ++j) {
+      const uint32_t w = s[j - j0];
+      const uint32_t d0 = 2u * j;
+      best = min(best, min(((w & 0xFFFFu) << 16) | d0, (w & 0xFFFF0000u) | (d0 + 1)));
+    }
+    if (j1 > j0) {
+      const uint32_t w = s[j1 - j0];
+      const uint32_t d0 = 2u * j1;
+      best = min(best, ((w & 0xFFFFu) << 16) | d0);
+      if ((int)d0 + 1 <= hi) best = min(best, (w & 0xFFFF0000u) | (d0 + 1));
+    }
+    wta_finish(a, s, lo, hi, j0, best, svl * HW + pix);
+  }
+}
+
+// u16 sums, 8 lanes per pixel: the group streams the pixel's pairs in
+// coalesced 32-byte rows, reduces (value << 16 | d) keys with shuffles, and
+// one lane walks outward from the winner over L1-resident data.
+__global__ void __launch_bounds__(256) k_wta_var_u16g(WtaArgs a) {
+  const size_t HW = (size_t)a.W * a.H;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & 7;
+  const int svl = blockIdx.y;
+  if (wta_skip(a, svl)) return;   // block-uniform
+  const size_t stride = ((size_t)gridDim.x * blockDim.x) >> 3;
+  for (size_t pix = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+       pix - ((threadIdx.x & 31) >> 3) < HW; pix += stride) {   // warp-uniform bound
+    const bool ok = pix < HW;
+    const uint2 mt = ok ? a.meta[svl * HW + pix] : make_uint2(0u, 0u);
+    const int lo = lo_of(mt), hi = hi_of(mt);
+    const int j0 = lo >> 1, j1 = hi >> 1;
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(a.S) + svl * a.volcap + mt.y;
+    uint32_t best = 0xFFFFFFFFu;
+    if (ok) {
+      for (int j = j0 + gl; j <= j1; j += 8) {
+        const uint32_t w = s[j - j0];
+        const uint32_t d0 = 2u * j;
+        if ((int)d0 >= lo) best = min(best, ((w & 0xFFFFu) << 16) | d0);
+        if ((int)d0 + 1 <= hi) best = min(best, (w & 0xFFFF0000u) | (d0 + 1));
+      }
+    }
+#pragma unroll
+    for (int o = 4; o; o >>= 1) best = min(best, __shfl_xor_sync(FULL, best, o));
+    if (ok && gl == 0) wta_finish(a, s, lo, hi, j0, best, svl * HW + pix);
+  }
+}
+
 void launch_wta_variance(const WtaArgs& a, int n_sv, cudaStream_t st) {
   const size_t HW = (size_t)a.W * a.H;
   if (a.arith == ARITH_U16 && a.dstar_in == nullptr) {
-    k_wta_var_u16<<<dim3((unsigned)((HW + 255) / 256), n_sv), 256, 0, st>>>(a);
+    if (a.cells) {
+      WtaArgs lo = a, hi = a;
+      lo.select = 1;
+      hi.select = 2;
+      const unsigned g1 = (unsigned)std::min<size_t>((HW + 255) / 256, WTA_GRID);
+      const unsigned g8 = (unsigned)std::min<size_t>((HW * 8 + 255) / 256, WTA_GRID);
+      k_wta_var_u16<<<dim3(g1, n_sv), 256, 0, st>>>(lo);
+      k_wta_var_u16g<<<dim3(g8, n_sv), 256, 0, st>>>(hi);
+    } else {
+      const unsigned g1 = (unsigned)std::min<size_t>((HW + 255) / 256, WTA_GRID);
+      k_wta_var_u16<<<dim3(g1, n_sv), 256, 0, st>>>(a);
+    }
     return;
   }
   dim3 grid((unsigned)((HW + 7) / 8), n_sv);

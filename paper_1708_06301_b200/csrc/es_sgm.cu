@@ -594,6 +594,30 @@ static void launch_grp2(const SgmArgs& a, int nch_pairs, int fam, int sweeps, in
 // forms "right neighbours of the first pair" is also "left neighbours of the
 // second pair".
 
+// global-space accesses with predication in PTX: no generic addressing and
+// no divergent branch around the conditional stores
+__device__ __forceinline__ uint32_t ld_pred(const uint32_t* p, bool pred, uint32_t dflt) {
+  uint32_t v = dflt;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.u32 %0, [%1];\n\t}\n"
+      : "+r"(v)
+      : "l"(p), "r"((int)pred));
+  return v;
+}
+__device__ __forceinline__ uint32_t ldc_pred(const uint32_t* p, bool pred, uint32_t dflt) {
+  uint32_t v = dflt;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.u32 %0, [%1];\n\t}\n"
+      : "+r"(v)
+      : "l"(p), "r"((int)pred));
+  return v;
+}
+__device__ __forceinline__ void st_pred(uint32_t* p, uint32_t v, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.u32 [%0], %1;\n\t}\n" ::"l"(p),
+               "r"(v), "r"((int)pred)
+               : "memory");
+}
+
 template <int G, int NCH>
 __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp3(SgmArgs a, int fam, int sweeps,
                                                               int init) {
@@ -618,8 +642,6 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp3(SgmArgs a, int fam,
   const uint32_t* __restrict__ C =
       reinterpret_cast<const uint32_t*>(a.C) + (size_t)blockIdx.y * a.volcap;
   uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
-  asm volatile("" : "+l"(C));
-  asm volatile("" : "+l"(S));
   const uint32_t p1x2 = a.p1i * 0x10001u;
   const uint32_t p2 = a.p2i;
   const int len = fam == FAM_H ? W : H;
@@ -639,8 +661,10 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp3(SgmArgs a, int fam,
       if (t < len && grp_pixel(fam, bwd, ch, t, W, H, x, y)) return meta[(size_t)y * W + x];
       return make_uint2(NONE, 0u);
     };
+    // three meta batches in flight: a batch is loaded 2G steps before use
     uint2 mb_cur = load_meta(0);
     uint2 mb_next = load_meta(G);
+    uint2 mb_next2 = load_meta(2 * G);
     int tb = 0;
     auto info = [&](int tp) -> GrpStep {
       GrpStep s{0u, 0, 0u, 0u};
@@ -649,7 +673,8 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp3(SgmArgs a, int fam,
         if (tp == tb + G) {
           tb += G;
           mb_cur = mb_next;
-          mb_next = load_meta(tb + G);
+          mb_next = mb_next2;
+          mb_next2 = load_meta(tb + 2 * G);
         }
         const int r = tp - tb;
         const uint32_t mx = __shfl_sync(FULL, mb_cur.x, gbase | r);
@@ -669,10 +694,13 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp3(SgmArgs a, int fam,
     auto fetch = [&](const GrpStep& s, uint32_t (&cn)[2 * NCH], uint32_t (&sn)[2 * NCH], int c) {
       const uint32_t rel = (uint32_t)(c * CW + 2 * gl - s.j0);
       const bool in0 = rel < s.span, in1 = rel + 1 < s.span;
-      cn[2 * c] = in0 ? __ldg(C + (s.my + rel)) : INF16x2;
-      cn[2 * c + 1] = in1 ? __ldg(C + (s.my + rel + 1)) : INF16x2;
-      sn[2 * c] = (in0 && !init_sum) ? S[s.my + rel] : 0u;
-      sn[2 * c + 1] = (in1 && !init_sum) ? S[s.my + rel + 1] : 0u;
+      // offsets wrap in 32 bits: rel = -1 (first pair below the interval)
+      // makes the second pair's offset exactly my
+      const uint32_t k0 = s.my + rel, k1 = s.my + rel + 1u;
+      cn[2 * c] = ldc_pred(C + k0, in0, INF16x2);
+      cn[2 * c + 1] = ldc_pred(C + k1, in1, INF16x2);
+      sn[2 * c] = ld_pred(S + k0, in0 && !init_sum, 0u);
+      sn[2 * c + 1] = ld_pred(S + k1, in1 && !init_sum, 0u);
     };
     uint32_t prev[2 * NCH], cA[2 * NCH], sA[2 * NCH], cB[2 * NCH], sB[2 * NCH];
     GrpStep s0 = info(0);
@@ -717,8 +745,10 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp3(SgmArgs a, int fam,
           prev[2 * c + 1] = Lb;
           nmin = __vminu2(nmin, __vminu2(La, Lb));
           const uint32_t rel = (uint32_t)(c * CW + 2 * gl - cur.j0);
-          if (rel < cur.span) S[cur.my + rel] = init_sum ? La : __vadd2(sn[2 * c], La);
-          if (rel + 1 < cur.span) S[cur.my + rel + 1] = init_sum ? Lb : __vadd2(sn[2 * c + 1], Lb);
+          st_pred(S + (uint32_t)(cur.my + rel), init_sum ? La : __vadd2(sn[2 * c], La),
+                  rel < cur.span);
+          st_pred(S + (uint32_t)(cur.my + rel + 1u), init_sum ? Lb : __vadd2(sn[2 * c + 1], Lb),
+                  rel + 1 < cur.span);
         } else {
           prev[2 * c] = INF16x2;
           prev[2 * c + 1] = INF16x2;

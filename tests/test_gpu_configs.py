@@ -1,0 +1,100 @@
+"""Parity on scaled-down versions of BASELINE.json configs 3 and 4, against
+the CPU oracle (itself pinned to the reference by tests/golden):
+
+* config 4 shape class: D = 256 (d_max = 255, two-register u16 chunks, the
+  wide-interval kernels) on a 640x160 rig, 3 frames, forward motion;
+* config 3 features: independently moving boxes (per-frame scene), 2% salt
+  noise per view, long-ish horizon (6 frames) so fallback windows, LR
+  rejection and the Kalman adopt/drop rule all occur.
+
+Inputs come from the device renderer; the oracle sees the same bytes."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _render(rig, boxes_per_frame, poses, seed, scale):
+    import torch
+    from paper_1708_06301_b200 import _lib
+    rs = _lib.rig_struct(rig)
+    out = []
+    for boxes, pose in zip(boxes_per_frame, poses):
+        b = np.ascontiguousarray(boxes[None], np.float64)
+        p = np.ascontiguousarray(pose[None], np.float64)
+        s = np.array([seed], np.int64)
+        img = torch.empty((1, 2, rig.height, rig.width), dtype=torch.uint8, device="cuda")
+        _lib.call("es_render", ctypes.byref(rs), _lib.ptr(b), b.shape[1], _lib.ptr(p), _lib.ptr(s),
+                  1, ctypes.c_double(scale), 12, ctypes.c_void_p(img.data_ptr()), None,
+                  ctypes.c_void_p(0))
+        out.append(img.cpu().numpy()[0])
+    return out
+
+
+def _compare(rig, frames, motions, params=None):
+    from paper_1708_06301_b200 import core, pipeline
+    pipe = pipeline.DisparityPipeline(rig, params)
+    orc = O.OracleStereo(rig.f, rig.b, rig.cx, rig.cy, rig.width, rig.height, rig.d_max)
+    fractions = []
+    for k, (img, motion) in enumerate(zip(frames, motions)):
+        res = pipe.process_frame(core.GrayImage(img[0]), core.GrayImage(img[1]), motion)
+        want = orc.step(img[0], img[1], motion)
+        for view, name in ((0, "left"), (1, "right")):
+            iv = res.intervals_left if view == 0 else res.intervals_right
+            assert np.array_equal(iv.lo, want[name + "_iv"][0]), (k, name)
+            assert np.array_equal(iv.hi, want[name + "_iv"][1]), (k, name)
+            meas = res.measured_left if view == 0 else res.measured_right
+            var = res.measured_left_var if view == 0 else res.measured_right_var
+            assert np.array_equal(meas.values, want[name + "_meas"][0]), (k, name, "wta")
+            assert np.array_equal(var.values, want[name + "_meas"][1]), (k, name, "r")
+            keep = res.keep_left if view == 0 else res.keep_right
+            assert np.array_equal(keep, want[name + "_keep"]), (k, name, "keep")
+            fd = res.fused.left if view == 0 else res.fused.right
+            fp = res.fused.left_var if view == 0 else res.fused.right_var
+            assert np.array_equal(fd.valid, want[name + "_fused"][2]), (k, name)
+            np.testing.assert_allclose(fd.values, want[name + "_fused"][0], rtol=1e-9, atol=0)
+            np.testing.assert_allclose(fp.values, want[name + "_fused"][1], rtol=1e-9, atol=0)
+        fractions.append(res.search_fraction_left)
+        np.testing.assert_allclose(res.search_fraction_left, want["left_fraction"], rtol=1e-15)
+    return fractions
+
+
+@pytest.mark.slow
+def test_config4_class_d256():
+    from paper_1708_06301_b200 import core, scenes
+    rig = core.StereoRig(f=450.0, b=0.3, cx=319.5, cy=79.5, width=640, height=160, d_max=255)
+    boxes, poses, motions = scenes.sequence_spec(seed=404, n_frames=3, step=0.4,
+                                                 yaw_deg=1.0, z_range=(0.9, 8.0))
+    frames = _render(rig, [boxes] * 3, poses, seed=3, scale=0.02)
+    fr = _compare(rig, frames, motions)
+    assert fr[0] == 1.0 and fr[-1] < 1.0
+
+
+def test_config3_class_moving_boxes_and_salt_noise():
+    from paper_1708_06301_b200 import core, scenes
+    rig = core.StereoRig(f=180.0, b=0.54, cx=151.0, cy=46.0, width=310, height=94, d_max=40)
+    n = 6
+    boxes, poses, motions = scenes.sequence_spec(seed=303, n_frames=n, step=0.5,
+                                                 z_range=(4.0, 30.0))
+    rng = np.random.default_rng(33)
+    movers = [2, 3, 4]   # three boxes move independently of the ego-motion
+    vel = rng.uniform(-0.3, 0.3, (len(movers), 3)) * np.array([1.0, 0.0, 1.0])
+    per_frame = []
+    for k in range(n):
+        b = boxes.copy()
+        for i, bi in enumerate(movers):
+            b[bi, 0:2] += vel[i, 0] * k
+            b[bi, 4:6] += vel[i, 2] * k
+        per_frame.append(b)
+    frames = _render(rig, per_frame, poses, seed=5, scale=0.05)
+    for img in frames:   # 2% salt noise, independent per view
+        for v in range(2):
+            mask = rng.random(img[v].shape) < 0.02
+            img[v][mask] = 255
+    fr = _compare(rig, frames, motions)
+    assert fr[0] == 1.0 and min(fr[1:]) < 1.0

@@ -16,7 +16,8 @@ import numpy as np
 from .errors import DeviceUnavailableError, DeviceUnsupportedError, PointAtInfinityError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libegostereo_b200.so")
+# ES_LIB_PATH: load an alternative build of the same library (A/B profiling)
+LIB_PATH = os.environ.get("ES_LIB_PATH") or os.path.join(HERE, "libegostereo_b200.so")
 
 ES_OK, ES_ERR_VALUE, ES_ERR_POINT_AT_INFINITY, ES_ERR_NONPOSITIVE_D = 0, 1, 2, 3
 ES_ERR_CUDA, ES_ERR_UNSUPPORTED = 4, 5

@@ -45,7 +45,7 @@ int check_rig(const es_rig* r) {
       r->height < 2)
     return fail(ES_ERR_VALUE, "invalid StereoRig");
   if (r->d_max > 511) return fail(ES_ERR_UNSUPPORTED, "device path supports d_max <= 511");
-  if ((double)r->width * npairs_max(r->d_max) * r->height >= 4294967295.0)
+  if ((double)row_capacity(r->width, r->d_max) * r->height >= 4294967295.0)
     return fail(ES_ERR_UNSUPPORTED, "volume exceeds 2^32 pairs per view");
   return ES_OK;
 }
@@ -288,7 +288,7 @@ int es_ctx_create(int device, const es_rig* rig, const es_params* prm, int batch
   c->B = batch;
   c->arith = choose_arith(prm->p1, prm->p2, (double)prm->window * prm->window * 255.0);
   c->HW = (size_t)rig->width * rig->height;
-  c->volcap = (size_t)rig->height * rig->width * npairs_max(rig->d_max);
+  c->volcap = (size_t)rig->height * row_capacity(rig->width, rig->d_max);
   const size_t n = c->HW * 2 * batch;
   const size_t vol_words = c->volcap * 2 * batch * (c->arith == ARITH_F32 ? 2 : 1);
   int e = ES_OK;
@@ -782,7 +782,7 @@ extern "C" int es_matching_cost(const uint8_t* left, const uint8_t* right, int H
   int64_t* dl = s.up(lo, n);
   int64_t* dh = s.up(hi, n);
   uint2* meta = s.get<uint2>(n);
-  const size_t volcap = (size_t)H * W * npairs_max(d_max);
+  const size_t volcap = (size_t)H * row_capacity(W, d_max);
   uint32_t* C = s.get<uint32_t>(volcap);
   float* dense = s.get<float>(n * (d_max + 1));
   NEED(dl && dh && meta && C && dense);
@@ -823,7 +823,7 @@ int stage_volume(Scratch& s, const float* vol, int H, int W, int D, uint2** meta
   unsigned f = 0;
   CK(cudaMemcpy(&f, flags, sizeof(unsigned), cudaMemcpyDeviceToHost));
   const int f32 = f != 0;   // anything but clean finite integer costs -> f32 storage
-  const size_t volcap = (size_t)H * W * npairs_max(d_max);
+  const size_t volcap = (size_t)H * row_capacity(W, d_max);
   void* rag = f32 ? (void*)s.get<float2>(volcap) : (void*)s.get<uint32_t>(volcap);
   NEED(rag);
   launch_import_dense(dense, meta, W, H, D, f32, rag, 0);
@@ -837,7 +837,7 @@ int stage_volume(Scratch& s, const float* vol, int H, int W, int D, uint2** meta
 
 int aggregate_staged(Scratch& s, uint2* meta, void* rag, int f32, unsigned flags, const float* vol,
                      int H, int W, int D, double p1, double p2, void** S_out, int* arith_out) {
-  const size_t volcap = (size_t)H * W * npairs_max(D - 1);
+  const size_t volcap = (size_t)H * row_capacity(W, D - 1);
   double cmax = 0;
   if (!f32) {
     // integer costs: bound by the largest value present
@@ -918,7 +918,7 @@ int es_select_disparity(const float* vol, int H, int W, int D, double* d, uint8_
   wa.H = H;
   wa.meta = meta;
   wa.S = rag;
-  wa.volcap = (size_t)H * W * npairs_max(D - 1);
+  wa.volcap = (size_t)H * row_capacity(W, D - 1);
   wa.arith = f32 ? ARITH_F32 : ARITH_U16;
   wa.s_max = 1.0;
   wa.r_min = 1.0;
@@ -946,7 +946,7 @@ int es_matching_variance_map(const float* vol, const int64_t* lo, const int64_t*
   float* dense = s.up(vol, n * D);
   NEED(dl && dh && meta && dense);
   launch_meta_from_intervals(dl, dh, W, H, D - 1, meta, 0);
-  const size_t volcap = n * npairs_max(D - 1);
+  const size_t volcap = (size_t)H * row_capacity(W, D - 1);
   float2* rag = s.get<float2>(volcap);
   NEED(rag);
   launch_import_dense(dense, meta, W, H, D, 1, rag, 0);

@@ -40,6 +40,20 @@ constexpr int ERR_NONPOSITIVE_D = 2;
 
 __host__ __device__ inline int npairs_max(int d_max) { return (d_max >> 1) + 1; }
 
+// Storage of one pixel: its pairs start at an offset o + (j0 & 1) inside an
+// allocation of pixel_slots() pairs at an even offset o, so (offset - j0) is
+// even and the two pairs 2k, 2k+1 any lane holds form one aligned 8-byte word
+// inside the pixel's own allocation.
+__host__ __device__ inline uint32_t pixel_slots(int lo, int hi) {
+  const uint32_t j0 = (uint32_t)lo >> 1, j1 = (uint32_t)hi >> 1;
+  return (j1 - j0 + 1 + (j0 & 1) + 1) & ~1u;
+}
+// pairs reserved per image row (multiple of 4 so rows start 16-byte aligned)
+__host__ __device__ inline size_t row_capacity(int W, int d_max) {
+  const size_t per = (size_t)((npairs_max(d_max) + 1) & ~1);
+  return ((size_t)W * per + 3) & ~(size_t)3;
+}
+
 __device__ __forceinline__ uint32_t lo_of(uint2 m) { return m.x & 0xFFFFu; }
 __device__ __forceinline__ uint32_t hi_of(uint2 m) { return m.x >> 16; }
 

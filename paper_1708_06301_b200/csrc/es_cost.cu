@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(COST_NT) k_cost(CostArgs a) {
   const uint8_t* ref = a.img + ((size_t)seq * 2 + view) * HW;
   const uint8_t* oth = a.img + ((size_t)seq * 2 + (view ^ 1)) * HW;
   const uint2* meta = a.meta + (size_t)svl * HW + (size_t)y * W;
-  const uint32_t rowbase = (uint32_t)y * (uint32_t)(W * npairs_max(a.d_max));
+  const uint32_t rowbase = (uint32_t)(y * row_capacity(W, a.d_max));
   for (int x = threadIdx.x; x < W; x += COST_NT) {
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(COST_NT) k_cost_w3(CostArgs a) {
   const uint8_t* ref = a.img + ((size_t)seq * 2 + view) * HW;
   const uint8_t* oth = a.img + ((size_t)seq * 2 + (view ^ 1)) * HW;
   const uint2* meta = a.meta + (size_t)svl * HW + (size_t)y * W;
-  const uint32_t rowbase = (uint32_t)y * (uint32_t)(W * npairs_max(a.d_max));
+  const uint32_t rowbase = (uint32_t)(y * row_capacity(W, a.d_max));
   const int y0 = max(y - 1, 0), y2 = min(y + 1, H - 1);
   for (int x = threadIdx.x; x < W; x += COST_NT) {
     refcol[x] = (uint32_t)ref[(size_t)y0 * W + x] | ((uint32_t)ref[(size_t)y * W + x] << 8) |

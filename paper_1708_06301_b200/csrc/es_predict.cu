@@ -195,19 +195,20 @@ __global__ void __launch_bounds__(NT) k_fill_v_intervals(PredArgs a) {
     a.pv[i] = v;
     int lo, hi;
     interval_of(d, p, v, d_max, lo, hi);
-    my_pairs += (uint32_t)((hi >> 1) - (lo >> 1) + 1);
+    my_pairs += pixel_slots(lo, hi);
     my_cells += (unsigned long long)(hi - lo + 1);
     a.meta[i].x = (uint32_t)lo | ((uint32_t)hi << 16);
   }
   uint32_t total;
   uint32_t base = block_exclusive_scan<NT>(my_pairs, scan_smem, total);
-  // pass 2: offsets
-  const uint32_t rowbase = (uint32_t)y * (uint32_t)(W * npairs_max(d_max));
+  // pass 2: offsets (first pair at an even slot offset + (j0 & 1))
+  const uint32_t rowbase = (uint32_t)(y * row_capacity(W, d_max));
   for (int x = x0; x < x1; ++x) {
     const size_t i = sv * HW + (size_t)y * W + x;
     const uint32_t m = a.meta[i].x;
-    a.meta[i].y = rowbase + base;
-    base += ((m >> 16) >> 1) - ((m & 0xFFFFu) >> 1) + 1;
+    const int lo = m & 0xFFFFu, hi = m >> 16;
+    a.meta[i].y = rowbase + base + ((uint32_t)(lo >> 1) & 1u);
+    base += pixel_slots(lo, hi);
   }
   atomicAdd(&cells_smem, my_cells);
   __syncthreads();
@@ -232,17 +233,18 @@ __global__ void __launch_bounds__(NT) k_meta_from_intervals(const int64_t* __res
   for (int x = x0; x < x1; ++x) {
     const size_t i = (size_t)y * W + x;
     const uint32_t lo = (uint32_t)lo_in[i], hi = (uint32_t)hi_in[i];
-    my_pairs += (hi >> 1) - (lo >> 1) + 1;
+    my_pairs += pixel_slots((int)lo, (int)hi);
     meta[i].x = lo | (hi << 16);
   }
   uint32_t total;
   uint32_t base = block_exclusive_scan<NT>(my_pairs, scan_smem, total);
-  const uint32_t rowbase = (uint32_t)y * (uint32_t)(W * npairs_max(d_max));
+  const uint32_t rowbase = (uint32_t)(y * row_capacity(W, d_max));
   for (int x = x0; x < x1; ++x) {
     const size_t i = (size_t)y * W + x;
     const uint32_t m = meta[i].x;
-    meta[i].y = rowbase + base;
-    base += ((m >> 16) >> 1) - ((m & 0xFFFFu) >> 1) + 1;
+    const int lo = m & 0xFFFFu, hi = m >> 16;
+    meta[i].y = rowbase + base + ((uint32_t)(lo >> 1) & 1u);
+    base += pixel_slots(lo, hi);
   }
 }
 

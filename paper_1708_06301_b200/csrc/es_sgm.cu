@@ -612,6 +612,31 @@ __device__ __forceinline__ uint32_t ldc_pred(const uint32_t* p, bool pred, uint3
       : "l"(p), "r"((int)pred));
   return v;
 }
+// 8-byte variants: a lane's two pairs are one aligned word of its pixel's
+// allocation (see pixel_slots), so one access serves both
+__device__ __forceinline__ uint2 ld2_pred(const uint32_t* p, bool pred) {
+  uint32_t a = 0u, b = 0u;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q ld.global.v2.u32 {%0, %1}, [%2];\n\t}\n"
+      : "+r"(a), "+r"(b)
+      : "l"(p), "r"((int)pred));
+  return make_uint2(a, b);
+}
+__device__ __forceinline__ uint2 ldc2_pred(const uint32_t* p, bool pred) {
+  uint32_t a = INF16x2, b = INF16x2;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q ld.global.nc.v2.u32 {%0, %1}, [%2];\n\t}\n"
+      : "+r"(a), "+r"(b)
+      : "l"(p), "r"((int)pred));
+  return make_uint2(a, b);
+}
+__device__ __forceinline__ void st2_pred(uint32_t* p, uint32_t a, uint32_t b, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q st.global.v2.u32 [%0], {%1, %2};\n\t}\n" ::"l"(p),
+      "r"(a), "r"(b), "r"((int)pred)
+      : "memory");
+}
+
 __device__ __forceinline__ void st_pred(uint32_t* p, uint32_t v, bool pred) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.u32 [%0], %1;\n\t}\n" ::"l"(p),
                "r"(v), "r"((int)pred)
@@ -694,13 +719,25 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp3(SgmArgs a, int fam,
     auto fetch = [&](const GrpStep& s, uint32_t (&cn)[2 * NCH], uint32_t (&sn)[2 * NCH], int c) {
       const uint32_t rel = (uint32_t)(c * CW + 2 * gl - s.j0);
       const bool in0 = rel < s.span, in1 = rel + 1 < s.span;
-      // offsets wrap in 32 bits: rel = -1 (first pair below the interval)
-      // makes the second pair's offset exactly my
-      const uint32_t k0 = s.my + rel, k1 = s.my + rel + 1u;
+      // offsets wrap in 32 bits (rel = -1: first pair just below the
+      // interval); k0 is even, so both pairs are one aligned 8-byte word
+      const uint32_t k0 = s.my + rel;
+#ifndef ES_GRP3_SCALAR
+      // raw words: the out-of-interval half is masked where it is used, so
+      // nothing here waits for the load
+      const bool any = in0 || in1;
+      const uint2 cv = ldc2_pred(C + k0, any);
+      cn[2 * c] = cv.x;
+      cn[2 * c + 1] = cv.y;
+      const uint2 sv = ld2_pred(S + k0, any && !init_sum);
+      sn[2 * c] = sv.x;
+      sn[2 * c + 1] = sv.y;
+#else
       cn[2 * c] = ldc_pred(C + k0, in0, INF16x2);
-      cn[2 * c + 1] = ldc_pred(C + k1, in1, INF16x2);
+      cn[2 * c + 1] = ldc_pred(C + (uint32_t)(k0 + 1u), in1, INF16x2);
       sn[2 * c] = ld_pred(S + k0, in0 && !init_sum, 0u);
-      sn[2 * c + 1] = ld_pred(S + k1, in1 && !init_sum, 0u);
+      sn[2 * c + 1] = ld_pred(S + (uint32_t)(k0 + 1u), in1 && !init_sum, 0u);
+#endif
     };
     uint32_t prev[2 * NCH], cA[2 * NCH], sA[2 * NCH], cB[2 * NCH], sB[2 * NCH];
     GrpStep s0 = info(0);
@@ -739,16 +776,30 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp3(SgmArgs a, int fam,
           const uint32_t nbb = __vminu2(mid, __byte_perm(pb, pr, 0x5432));
           const uint32_t ca = __vminu2(__viaddmin_u16x2(nba, p1x2, pa), mp2);
           const uint32_t cb = __vminu2(__viaddmin_u16x2(nbb, p1x2, pb), mp2);
-          const uint32_t La = first ? cn[2 * c] : __vadd2(cn[2 * c], __vadd2(ca, ng));
-          const uint32_t Lb = first ? cn[2 * c + 1] : __vadd2(cn[2 * c + 1], __vadd2(cb, ng));
+          const uint32_t rel = (uint32_t)(c * CW + 2 * gl - cur.j0);
+#ifndef ES_GRP3_SCALAR
+          const uint32_t cwa = rel < cur.span ? cn[2 * c] : INF16x2;       // mask at use
+          const uint32_t cwb = rel + 1 < cur.span ? cn[2 * c + 1] : INF16x2;
+#else
+          const uint32_t cwa = cn[2 * c], cwb = cn[2 * c + 1];
+#endif
+          const uint32_t La = first ? cwa : __vadd2(cwa, __vadd2(ca, ng));
+          const uint32_t Lb = first ? cwb : __vadd2(cwb, __vadd2(cb, ng));
           prev[2 * c] = La;
           prev[2 * c + 1] = Lb;
           nmin = __vminu2(nmin, __vminu2(La, Lb));
-          const uint32_t rel = (uint32_t)(c * CW + 2 * gl - cur.j0);
+          // one 8-byte store; a half outside the interval lands in the
+          // pixel's own padding / out-of-interval slot, which nothing reads
+#ifndef ES_GRP3_SCALAR
+          st2_pred(S + (uint32_t)(cur.my + rel), init_sum ? La : __vadd2(sn[2 * c], La),
+                   init_sum ? Lb : __vadd2(sn[2 * c + 1], Lb),
+                   rel < cur.span || rel + 1 < cur.span);
+#else
           st_pred(S + (uint32_t)(cur.my + rel), init_sum ? La : __vadd2(sn[2 * c], La),
                   rel < cur.span);
           st_pred(S + (uint32_t)(cur.my + rel + 1u), init_sum ? Lb : __vadd2(sn[2 * c + 1], Lb),
                   rel + 1 < cur.span);
+#endif
         } else {
           prev[2 * c] = INF16x2;
           prev[2 * c + 1] = INF16x2;

@@ -807,14 +807,11 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp3(SgmArgs a, int fam,
         left_old = pb;
         if ((nn.um >> c) & 1u) fetch(nn, cn, sn, c);
       }
-      const uint32_t hm = min(nmin & 0xFFFFu, nmin >> 16);
-      uint32_t mg = 0;
+      // per-chain minimum: xor butterfly inside each G-lane group
+      uint32_t hm = min(nmin & 0xFFFFu, nmin >> 16);
 #pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        const uint32_t r = __reduce_min_sync(FULL, grp == g ? hm : 0xFFFFFFFFu);
-        if (grp == g) mg = r;
-      }
-      m = mg;
+      for (int o = G / 2; o; o >>= 1) hm = min(hm, __shfl_xor_sync(FULL, hm, o));
+      m = hm;
       was_active = act;
     };
     for (int t = 0; t < len; t += 2) {
@@ -1123,7 +1120,7 @@ void launch_aggregate_split(const SgmArgs& a, int n_sv, cudaStream_t st_lo, cuda
   const int np = npairs_max(a.d_max);
   const int fams[4] = {FAM_H, FAM_V, FAM_D1, FAM_D2};
   for (int k = 0; k < 4; ++k) {
-    launch_v4<8>(lo, fams[k], 3, k == 0, n_sv, st_lo);
+    launch_grp3<4>(lo, np, fams[k], 3, k == 0, n_sv, st_lo);
     launch_grp3<8>(hi, np, fams[k], 3, k == 0, n_sv, st_hi);
   }
 }

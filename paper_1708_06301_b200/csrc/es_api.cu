@@ -467,6 +467,9 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   // device from this frame's searched-cell count
   sa.lanes = c->lanes;
   sa.cells = c->cells;
+  // measured: the 4-lane kernel wins up to ~60% search fraction
+  static const double split = getenv("ES_SGM_SPLIT") ? atof(getenv("ES_SGM_SPLIT")) : 0.6;
+  sa.split = split;
   if (c->arith == ARITH_U16 && !c->lanes && getenv("ES_SGM_VAR") == nullptr) {
     // fork: wide-interval (seq, view)s run concurrently on the side stream
     CK(cudaEventRecord(c->ev_fork, c->st));

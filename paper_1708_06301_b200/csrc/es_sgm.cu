@@ -644,7 +644,10 @@ __device__ __forceinline__ void st_pred(uint32_t* p, uint32_t v, bool pred) {
 }
 
 template <int G, int NCH>
-__global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp3(SgmArgs a, int fam, int sweeps,
+// measured: capping the 4-lane instance at 128 registers (4 blocks/SM) wins
+// more from occupancy than it loses to one spilled word; the 8-lane instance
+// is fastest uncapped
+__global__ void __launch_bounds__(GRP_WARPS * 32, (G == 4 ? 4 : 1)) k_sgm_grp3(SgmArgs a, int fam, int sweeps,
                                                               int init) {
   constexpr int NG = 32 / G;
   constexpr int CW = 2 * G;   // pairs per chunk

@@ -163,6 +163,8 @@ struct es_ctx {
   uint8_t* pv = nullptr;
   unsigned long long* zkey = nullptr;
   uint32_t* zidx = nullptr;
+  uint32_t* wt = nullptr;
+  double* wd = nullptr;
   uint2* meta = nullptr;
   uint32_t *C = nullptr, *S = nullptr;
   uint16_t* dstar = nullptr;
@@ -209,7 +211,8 @@ int ctx_free(es_ctx* c) {
   if (!c) return ES_OK;
   cudaSetDevice(c->device);
   void* ptrs[] = {c->img, c->sd[0], c->sd[1], c->sp[0], c->sp[1], c->sv[0], c->sv[1], c->hd,
-                  c->hp, c->hv, c->pd, c->pp, c->pv, c->zkey, c->zidx, c->meta, c->C, c->S,
+                  c->hp, c->hv, c->pd, c->pp, c->pv, c->zkey, c->zidx, c->wt, c->wd, c->meta,
+                  c->C, c->S,
                   c->dstar, c->r, c->mvalid, c->keep, c->Hm, c->have_pred, c->err, c->anyv,
                   c->cells, c->kitti, c->cells_acc};
   for (void* p : ptrs)
@@ -240,6 +243,8 @@ PredArgs pred_args(es_ctx* c) {
   a.sv = c->sv[c->cur];
   a.zkey = c->zkey;
   a.zidx = c->zidx;
+  a.wt = c->wt;
+  a.wd = c->wd;
   a.hd = c->hd;
   a.hp = c->hp;
   a.hv = c->hv;
@@ -306,6 +311,8 @@ int es_ctx_create(int device, const es_rig* rig, const es_params* prm, int batch
   if (!e) e = dalloc(&c->pv, n);
   if (!e) e = dalloc(&c->zkey, n);
   if (!e) e = dalloc(&c->zidx, n);
+  if (!e) e = dalloc(&c->wt, n);
+  if (!e) e = dalloc(&c->wd, n);
   if (!e) e = dalloc(&c->meta, n);
   if (!e) e = dalloc(&c->C, c->volcap * 2 * batch);
   if (!e) e = dalloc(&c->S, vol_words);
@@ -1055,6 +1062,8 @@ int es_predict_view(const double* d, const double* p, const uint8_t* valid, cons
   a.sv = s.up(valid, n);
   a.zkey = s.get<unsigned long long>(n);
   a.zidx = s.get<uint32_t>(n);
+  a.wt = s.get<uint32_t>(n);
+  a.wd = s.get<double>(n);
   a.hd = s.get<double>(n);
   a.hp = s.get<double>(n);
   a.hv = s.get<uint8_t>(n);
@@ -1064,7 +1073,8 @@ int es_predict_view(const double* d, const double* p, const uint8_t* valid, cons
   a.meta = nullptr;
   a.cells = nullptr;
   a.err = s.get<int>(1);
-  NEED(a.Hm && a.have_pred && a.sd && a.sp && a.sv && a.zkey && a.zidx && a.hd && a.hp && a.hv &&
+  NEED(a.Hm && a.have_pred && a.sd && a.sp && a.sv && a.zkey && a.zidx && a.wt && a.wd && a.hd &&
+       a.hp && a.hv &&
        a.err);
   CK(cudaMemset(a.err, 0, sizeof(int)));
   launch_predict(a, 1, 0);

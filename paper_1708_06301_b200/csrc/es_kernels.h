@@ -18,6 +18,8 @@ struct PredArgs {
   const uint8_t* sv;
   unsigned long long* zkey;  // z-buffer phase 1 (bits of max d')
   uint32_t* zidx;            // z-buffer phase 2 (min source index)
+  uint32_t* wt;              // per source: landing pixel (NO_SRC: not splatted)
+  double* wd;                // per source: warped disparity d'
   double* hd;                // after the horizontal fill pass
   double* hp;
   uint8_t* hv;

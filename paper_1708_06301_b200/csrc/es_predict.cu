@@ -63,20 +63,26 @@ __global__ void k_warp_zmax(PredArgs a) {
   if (i >= (int)HW) return;
   const double* d = a.sd + sv * HW;
   const uint8_t* v = a.sv + sv * HW;
-  if (!v[i]) return;
-  const int x = i % a.rig.W, y = i / a.rig.W;
-  if (a.prm.edge_reject && is_edge(d, v, x, y, a.rig.W, a.rig.H, a.prm.edge_window, a.prm.gamma_e))
-    return;
-  uint32_t tgt;
-  double dp;
-  bool at_inf;
-  const double di = d[i];
-  if (!warp_src(a.Hm + 16 * sv, a.rig, x, y, di, tgt, dp, at_inf)) {
-    if (at_inf) atomicOr(a.err + s, ERR_POINT_AT_INFINITY);
-    return;
+  uint32_t tgt = NO_SRC;
+  double dp = 0.0;
+  if (v[i]) {
+    const int x = i % a.rig.W, y = i / a.rig.W;
+    if (!(a.prm.edge_reject &&
+          is_edge(d, v, x, y, a.rig.W, a.rig.H, a.prm.edge_window, a.prm.gamma_e))) {
+      bool at_inf;
+      const double di = d[i];
+      if (warp_src(a.Hm + 16 * sv, a.rig, x, y, di, tgt, dp, at_inf)) {
+        if (!(di > 0.0)) atomicOr(a.err + s, ERR_NONPOSITIVE_D);
+        atomicMax(a.zkey + sv * HW + tgt, (unsigned long long)__double_as_longlong(dp));
+      } else {
+        tgt = NO_SRC;
+        if (at_inf) atomicOr(a.err + s, ERR_POINT_AT_INFINITY);
+      }
+    }
   }
-  if (!(di > 0.0)) atomicOr(a.err + s, ERR_NONPOSITIVE_D);
-  atomicMax(a.zkey + sv * HW + tgt, (unsigned long long)__double_as_longlong(dp));
+  // the landing of every source, so later passes never recompute the warp
+  a.wt[sv * HW + i] = tgt;
+  a.wd[sv * HW + i] = dp;
 }
 
 __global__ void k_warp_zidx(PredArgs a) {
@@ -86,16 +92,9 @@ __global__ void k_warp_zidx(PredArgs a) {
   const size_t HW = (size_t)a.rig.W * a.rig.H;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int)HW) return;
-  const double* d = a.sd + sv * HW;
-  const uint8_t* v = a.sv + sv * HW;
-  if (!v[i]) return;
-  const int x = i % a.rig.W, y = i / a.rig.W;
-  if (a.prm.edge_reject && is_edge(d, v, x, y, a.rig.W, a.rig.H, a.prm.edge_window, a.prm.gamma_e))
-    return;
-  uint32_t tgt;
-  double dp;
-  bool at_inf;
-  if (!warp_src(a.Hm + 16 * sv, a.rig, x, y, d[i], tgt, dp, at_inf)) return;
+  const uint32_t tgt = a.wt[sv * HW + i];
+  if (tgt == NO_SRC) return;
+  const double dp = a.wd[sv * HW + i];
   if ((unsigned long long)__double_as_longlong(dp) == a.zkey[sv * HW + tgt])
     atomicMin(a.zidx + sv * HW + tgt, (uint32_t)i);
 }
@@ -112,10 +111,7 @@ __device__ __forceinline__ void resolve(const PredArgs& a, int sv, uint32_t t, d
   if (src == NO_SRC) return;
   const double d = a.sd[sv * HW + src];
   const double p = a.sp[sv * HW + src];
-  uint32_t tgt;
-  double dp;
-  bool at_inf;
-  warp_src(a.Hm + 16 * sv, a.rig, (int)(src % a.rig.W), (int)(src / a.rig.W), d, tgt, dp, at_inf);
+  const double dp = a.wd[sv * HW + src];
   const double ratio = dp / d;
   od = dp;
   op = ratio * ratio * p + a.prm.q;

@@ -46,6 +46,19 @@ TEXTURE_SCALE = 0.05
 KERNELS_PER_STEP = 15   # zmax, zidx, fill_h, fill_v, cost, 4 families x 2 sgm variants, wta, fuse
 
 
+def measured_traffic(batch, texture_scale):
+    """DRAM bytes per step of the aggregation stage from the committed ncu
+    capture of the same workload (profiles/r01/agg_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "agg_traffic.json")) as fh:
+            t = json.load(fh)
+        if t["batch"] == batch and abs(t["texture_scale"] - texture_scale) < 1e-12:
+            return float(t["dram_bytes_per_step"])
+    except Exception:
+        pass
+    return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -303,8 +316,12 @@ def main():
         "stage_ms_per_step": {n: stage[i] / max(nsteps.value, 1) for i, n in enumerate(stage_names)},
         "roofline": {"bound": "hbm", "kernel": "sgm aggregation (4 family launches)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                     "bytes_per_step": agg_bytes},
+                     "frac": achieved / peak,
+                     # ncu DRAM bytes of the same stage per step (committed capture of
+                     # this workload), vs bytes_per_step algorithmic
+                     "traffic": measured_traffic(B, TEXTURE_SCALE),
+                     "traffic_unit": "bytes per step (all sequences, both views)",
+                     "peak_kind": peak_kind, "bytes_per_step": agg_bytes},
         "pipeline_roofline": {"achieved": frame_bytes / (ms_max / K / 1e3) / 1e9,
                               "frac": frame_bytes / (ms_max / K / 1e3) / 1e9 / peak},
         "gpu_launches": KERNELS_PER_STEP * K,

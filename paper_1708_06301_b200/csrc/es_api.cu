@@ -151,6 +151,9 @@ struct es_ctx {
   size_t HW = 0, volcap = 0;
   cudaStream_t st = nullptr;
   cudaStream_t st2 = nullptr;          // side stream for concurrent SGM variants
+  cudaStream_t st3 = nullptr, st4 = nullptr;   // second partial-sum family streams
+  uint32_t* S2 = nullptr;              // second u16 partial sum (V + D2 families)
+  bool s2_live = false;                // the last step's total is S + S2
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   uint8_t* img = nullptr;
   double* sd[2] = {nullptr, nullptr};
@@ -213,7 +216,7 @@ int ctx_free(es_ctx* c) {
   void* ptrs[] = {c->img, c->sd[0], c->sd[1], c->sp[0], c->sp[1], c->sv[0], c->sv[1], c->hd,
                   c->hp, c->hv, c->pd, c->pp, c->pv, c->zkey, c->zidx, c->wt, c->wd, c->meta,
                   c->C, c->S,
-                  c->dstar, c->r, c->mvalid, c->keep, c->Hm, c->have_pred, c->err, c->anyv,
+                  c->S2, c->dstar, c->r, c->mvalid, c->keep, c->Hm, c->have_pred, c->err, c->anyv,
                   c->cells, c->kitti, c->cells_acc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -226,6 +229,8 @@ int ctx_free(es_ctx* c) {
     for (cudaEvent_t e : a) cudaEventDestroy(e);
   if (c->st) cudaStreamDestroy(c->st);
   if (c->st2) cudaStreamDestroy(c->st2);
+  if (c->st3) cudaStreamDestroy(c->st3);
+  if (c->st4) cudaStreamDestroy(c->st4);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
@@ -316,6 +321,7 @@ int es_ctx_create(int device, const es_rig* rig, const es_params* prm, int batch
   if (!e) e = dalloc(&c->meta, n);
   if (!e) e = dalloc(&c->C, c->volcap * 2 * batch);
   if (!e) e = dalloc(&c->S, vol_words);
+  if (!e && c->arith == ARITH_U16) e = dalloc(&c->S2, vol_words);
   if (!e) e = dalloc(&c->dstar, n);
   if (!e) e = dalloc(&c->r, n);
   if (!e) e = dalloc(&c->mvalid, n);
@@ -343,6 +349,8 @@ int es_ctx_create(int device, const es_rig* rig, const es_params* prm, int batch
       cudaMallocHost(&c->h_cells, sizeof(unsigned long long) * 2 * batch) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->st4, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     ctx_free(c);
@@ -477,23 +485,31 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   // measured: the 4-lane kernel wins up to ~60% search fraction
   static const double split = getenv("ES_SGM_SPLIT") ? atof(getenv("ES_SGM_SPLIT")) : 0.6;
   sa.split = split;
+  static const bool two_sums = !(getenv("ES_SGM_S2") && atoi(getenv("ES_SGM_S2")) == 0);
+  const bool use_s2 = two_sums && c->S2 != nullptr;
   if (c->arith == ARITH_U16 && !c->lanes && getenv("ES_SGM_VAR") == nullptr) {
-    // fork: wide-interval (seq, view)s run concurrently on the side stream
+    // fork: wide-interval (seq, view)s run concurrently on a side stream and,
+    // with two partial sums, the column/anti-diagonal families on two more
     CK(cudaEventRecord(c->ev_fork, c->st));
-    CK(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
-    launch_aggregate_split(sa, n_sv, c->st, c->st2);
-    CK(cudaEventRecord(c->ev_join, c->st2));
-    CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
+    cudaStream_t side[3] = {c->st2, c->st3, c->st4};
+    for (cudaStream_t s : side) CK(cudaStreamWaitEvent(s, c->ev_fork, 0));
+    launch_aggregate_split(sa, n_sv, c->st, c->st2, use_s2 ? c->S2 : nullptr, c->st3, c->st4);
+    for (cudaStream_t s : side) {
+      CK(cudaEventRecord(c->ev_join, s));
+      CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
+    }
   } else {
     launch_aggregate(sa, c->arith, n_sv, c->st);
   }
   mark(4);
+  c->s2_live = use_s2 && c->arith == ARITH_U16 && !c->lanes && getenv("ES_SGM_VAR") == nullptr;
 
   WtaArgs wa;
   wa.W = c->rig.W;
   wa.H = c->rig.H;
   wa.meta = c->meta;
   wa.S = c->S;
+  wa.S2 = c->s2_live ? c->S2 : nullptr;
   wa.volcap = c->volcap;
   wa.arith = c->arith;
   wa.s_max = c->prm.s_max;
@@ -674,7 +690,8 @@ int es_ctx_export(es_ctx* c, int what, int seq, int view, void* out) {
                             c->arith == ARITH_F32 ? (void*)((float2*)c->S + sv * c->volcap)
                                                   : (void*)(c->S + sv * c->volcap),
                             c->arith == ARITH_F32 ? EXPORT_F32 : EXPORT_U16_SUM, c->rig.W,
-                            c->rig.H, c->rig.d_max, (float*)tmp, c->st);
+                            c->rig.H, c->rig.d_max, (float*)tmp, c->st,
+                            c->s2_live ? (const void*)(c->S2 + sv * c->volcap) : nullptr);
       src = tmp;
       bytes = sizeof(float) * n;
       break;

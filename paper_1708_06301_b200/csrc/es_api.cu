@@ -150,10 +150,13 @@ struct es_ctx {
   int arith = ARITH_U16;
   size_t HW = 0, volcap = 0;
   cudaStream_t st = nullptr;
-  cudaStream_t st2 = nullptr;          // side stream for concurrent SGM variants
-  cudaStream_t st3 = nullptr, st4 = nullptr;   // second partial-sum family streams
-  uint32_t* S2 = nullptr;              // second u16 partial sum (V + D2 families)
-  bool s2_live = false;                // the last step's total is S + S2
+  // concurrent SGM: families accumulate into `parts` u16 partial sums (S and
+  // Sx[0..parts-2]); reduced- and wide-interval variants of partial p run on
+  // streams lo[p] / hi[p] (lo[0] = st)
+  int parts = 1;
+  uint32_t* Sx[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t sx[7] = {};
+  int parts_live = 1;                  // partial sums holding the last step's total
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   uint8_t* img = nullptr;
   double* sd[2] = {nullptr, nullptr};
@@ -216,7 +219,8 @@ int ctx_free(es_ctx* c) {
   void* ptrs[] = {c->img, c->sd[0], c->sd[1], c->sp[0], c->sp[1], c->sv[0], c->sv[1], c->hd,
                   c->hp, c->hv, c->pd, c->pp, c->pv, c->zkey, c->zidx, c->wt, c->wd, c->meta,
                   c->C, c->S,
-                  c->S2, c->dstar, c->r, c->mvalid, c->keep, c->Hm, c->have_pred, c->err, c->anyv,
+                  c->Sx[0], c->Sx[1], c->Sx[2], c->dstar, c->r, c->mvalid, c->keep, c->Hm,
+                  c->have_pred, c->err, c->anyv,
                   c->cells, c->kitti, c->cells_acc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -228,9 +232,8 @@ int ctx_free(es_ctx* c) {
   for (auto& a : c->prof)
     for (cudaEvent_t e : a) cudaEventDestroy(e);
   if (c->st) cudaStreamDestroy(c->st);
-  if (c->st2) cudaStreamDestroy(c->st2);
-  if (c->st3) cudaStreamDestroy(c->st3);
-  if (c->st4) cudaStreamDestroy(c->st4);
+  for (cudaStream_t s : c->sx)
+    if (s) cudaStreamDestroy(s);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
@@ -321,7 +324,14 @@ int es_ctx_create(int device, const es_rig* rig, const es_params* prm, int batch
   if (!e) e = dalloc(&c->meta, n);
   if (!e) e = dalloc(&c->C, c->volcap * 2 * batch);
   if (!e) e = dalloc(&c->S, vol_words);
-  if (!e && c->arith == ARITH_U16) e = dalloc(&c->S2, vol_words);
+  if (c->arith == ARITH_U16) {
+    // small batches are latency-bound: one partial sum (and stream) per path
+    // family; large ones use two (measured)
+    const char* pe = getenv("ES_SGM_PARTS");
+    c->parts = pe ? atoi(pe) : (batch <= 8 ? 4 : 2);
+    if (c->parts != 1 && c->parts != 2 && c->parts != 4) c->parts = 2;
+    for (int p = 0; p + 1 < c->parts && !e; ++p) e = dalloc(&c->Sx[p], vol_words);
+  }
   if (!e) e = dalloc(&c->dstar, n);
   if (!e) e = dalloc(&c->r, n);
   if (!e) e = dalloc(&c->mvalid, n);
@@ -348,9 +358,13 @@ int es_ctx_create(int device, const es_rig* rig, const es_params* prm, int batch
       cudaMallocHost(&c->h_anyv, sizeof(int) * batch) != cudaSuccess ||
       cudaMallocHost(&c->h_cells, sizeof(unsigned long long) * 2 * batch) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->st4, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->sx[0], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->sx[1], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->sx[2], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->sx[3], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->sx[4], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->sx[5], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->sx[6], cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     ctx_free(c);
@@ -485,31 +499,39 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   // measured: the 4-lane kernel wins up to ~60% search fraction
   static const double split = getenv("ES_SGM_SPLIT") ? atof(getenv("ES_SGM_SPLIT")) : 0.6;
   sa.split = split;
-  static const bool two_sums = !(getenv("ES_SGM_S2") && atoi(getenv("ES_SGM_S2")) == 0);
-  const bool use_s2 = two_sums && c->S2 != nullptr;
   if (c->arith == ARITH_U16 && !c->lanes && getenv("ES_SGM_VAR") == nullptr) {
-    // fork: wide-interval (seq, view)s run concurrently on a side stream and,
-    // with two partial sums, the column/anti-diagonal families on two more
+    // fork: the partial sums' families and the two regime variants run on
+    // 2 * parts concurrent streams; each touches its own (seq, view) x sum
+    const int P = c->parts;
+    void* S[4] = {c->S, c->Sx[0], c->Sx[1], c->Sx[2]};
+    const cudaStream_t lo[4] = {c->st, c->sx[1], c->sx[3], c->sx[5]};
+    const cudaStream_t hi[4] = {c->sx[0], c->sx[2], c->sx[4], c->sx[6]};
     CK(cudaEventRecord(c->ev_fork, c->st));
-    cudaStream_t side[3] = {c->st2, c->st3, c->st4};
-    for (cudaStream_t s : side) CK(cudaStreamWaitEvent(s, c->ev_fork, 0));
-    launch_aggregate_split(sa, n_sv, c->st, c->st2, use_s2 ? c->S2 : nullptr, c->st3, c->st4);
-    for (cudaStream_t s : side) {
-      CK(cudaEventRecord(c->ev_join, s));
-      CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
+    for (int p = 0; p < P; ++p) {
+      if (p) CK(cudaStreamWaitEvent(lo[p], c->ev_fork, 0));
+      CK(cudaStreamWaitEvent(hi[p], c->ev_fork, 0));
     }
+    launch_aggregate_parts(sa, n_sv, P, S, lo, hi);
+    for (int p = 0; p < P; ++p) {
+      for (cudaStream_t s : {lo[p], hi[p]}) {
+        if (s == c->st) continue;
+        CK(cudaEventRecord(c->ev_join, s));
+        CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
+      }
+    }
+    c->parts_live = P;
   } else {
     launch_aggregate(sa, c->arith, n_sv, c->st);
+    c->parts_live = 1;
   }
   mark(4);
-  c->s2_live = use_s2 && c->arith == ARITH_U16 && !c->lanes && getenv("ES_SGM_VAR") == nullptr;
 
   WtaArgs wa;
   wa.W = c->rig.W;
   wa.H = c->rig.H;
   wa.meta = c->meta;
   wa.S = c->S;
-  wa.S2 = c->s2_live ? c->S2 : nullptr;
+  for (int p = 1; p < c->parts_live; ++p) wa.Sx[p - 1] = c->Sx[p - 1];
   wa.volcap = c->volcap;
   wa.arith = c->arith;
   wa.s_max = c->prm.s_max;
@@ -691,7 +713,9 @@ int es_ctx_export(es_ctx* c, int what, int seq, int view, void* out) {
                                                   : (void*)(c->S + sv * c->volcap),
                             c->arith == ARITH_F32 ? EXPORT_F32 : EXPORT_U16_SUM, c->rig.W,
                             c->rig.H, c->rig.d_max, (float*)tmp, c->st,
-                            c->s2_live ? (const void*)(c->S2 + sv * c->volcap) : nullptr);
+                            c->parts_live > 1 ? (const void*)(c->Sx[0] + sv * c->volcap) : nullptr,
+                            c->parts_live > 2 ? (const void*)(c->Sx[1] + sv * c->volcap) : nullptr,
+                            c->parts_live > 3 ? (const void*)(c->Sx[2] + sv * c->volcap) : nullptr);
       src = tmp;
       bytes = sizeof(float) * n;
       break;

@@ -74,11 +74,11 @@ struct SgmArgs {
 // full 8-path aggregation; the u16 path runs 4 family launches (both sweeps
 // each), the f32 path runs the 8 directions in the reference's order
 void launch_aggregate(const SgmArgs& a, int arith, int n_sv, cudaStream_t st);
-// u16 only, a.cells required: reduced-interval (seq, view)s on st_lo, wide ones on st_hi;
-// with S2 != nullptr the V and D2 families accumulate into S2 on st_lo2 / st_hi2
-void launch_aggregate_split(const SgmArgs& a, int n_sv, cudaStream_t st_lo, cudaStream_t st_hi,
-                            void* S2 = nullptr, cudaStream_t st_lo2 = nullptr,
-                            cudaStream_t st_hi2 = nullptr);
+// u16 only, a.cells required: the 4 path families accumulate into `parts`
+// (1, 2 or 4) partial sums S[k % parts]; reduced-interval (seq, view)s run on
+// st_lo[p], wide ones on st_hi[p]; all streams may run concurrently
+void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S,
+                            const cudaStream_t* st_lo, const cudaStream_t* st_hi);
 
 struct WtaArgs {
   int W, H;
@@ -91,7 +91,7 @@ struct WtaArgs {
   double* r;
   uint8_t* valid;
   const uint16_t* dstar_in = nullptr;  // optional caller winners (variance only)
-  const void* S2 = nullptr;            // optional second u16 partial sum (added to S)
+  const void* Sx[3] = {nullptr, nullptr, nullptr};  // further u16 partial sums (added to S)
   // optional per-(seq, view) kernel choice as in SgmArgs: thread per pixel for
   // reduced intervals, 8 lanes per pixel for wide ones
   const unsigned long long* cells = nullptr;
@@ -104,7 +104,8 @@ void launch_wta_variance(const WtaArgs& a, int n_sv, cudaStream_t st);
 // dense <-> ragged converters for parity export and stage-level APIs
 enum ExportMode { EXPORT_U16_COST = 0, EXPORT_F32 = 1, EXPORT_U16_SUM = 2 };
 void launch_export_dense(const uint2* meta, const void* vol, int vol_f32, int W, int H, int d_max,
-                         float* out, cudaStream_t st, const void* vol2 = nullptr);
+                         float* out, cudaStream_t st, const void* vol2 = nullptr,
+                         const void* vol3 = nullptr, const void* vol4 = nullptr);
 void launch_import_dense(const float* dense, const uint2* meta, int W, int H, int D, int as_f32,
                          void* vol, cudaStream_t st);
 void launch_hull(const float* dense, int W, int H, int D, int64_t* lo, int64_t* hi,

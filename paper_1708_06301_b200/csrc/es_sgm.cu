@@ -1116,33 +1116,23 @@ static void launch_family(const SgmArgs& a, int nch, int fam, int sweeps, int in
 // reduced intervals run the v4 kernel on st_lo, wide ones the 2-pairs/lane
 // kernel on st_hi; each (seq, view) is handled by exactly one stream, so the
 // two streams never touch the same volume and run concurrently
-void launch_aggregate_split(const SgmArgs& a, int n_sv, cudaStream_t st_lo, cudaStream_t st_hi,
-                            void* S2, cudaStream_t st_lo2, cudaStream_t st_hi2) {
-  SgmArgs lo = a, hi = a;
-  lo.select = 1;
-  hi.select = 2;
+void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S,
+                            const cudaStream_t* st_lo, const cudaStream_t* st_hi) {
+  // parts partial sums: family k accumulates into S[k % parts] on streams
+  // st_lo/st_hi[k % parts]; each (seq, view) uses exactly one of lo / hi
   const int np = npairs_max(a.d_max);
-  if (S2 == nullptr) {
-    const int fams[4] = {FAM_H, FAM_V, FAM_D1, FAM_D2};
-    for (int k = 0; k < 4; ++k) {
-      launch_grp3<4>(lo, np, fams[k], 3, k == 0, n_sv, st_lo);
-      launch_grp3<8>(hi, np, fams[k], 3, k == 0, n_sv, st_hi);
-    }
-    return;
+  const int fams[4] = {FAM_H, FAM_V, FAM_D1, FAM_D2};
+  for (int k = 0; k < 4; ++k) {
+    const int p = k % parts;
+    SgmArgs lo = a, hi = a;
+    lo.select = 1;
+    hi.select = 2;
+    lo.S = S[p];
+    hi.S = S[p];
+    const int init = k < parts;   // first family into this partial sum
+    launch_grp3<4>(lo, np, fams[k], 3, init, n_sv, st_lo[p]);
+    launch_grp3<8>(hi, np, fams[k], 3, init, n_sv, st_hi[p]);
   }
-  // two partial sums: rows + x-y diagonals into S, columns + x+y diagonals
-  // into S2, on separate streams, so the long row chains overlap the rest
-  SgmArgs lo2 = lo, hi2 = hi;
-  lo2.S = S2;
-  hi2.S = S2;
-  launch_grp3<4>(lo, np, FAM_H, 3, 1, n_sv, st_lo);
-  launch_grp3<8>(hi, np, FAM_H, 3, 1, n_sv, st_hi);
-  launch_grp3<4>(lo2, np, FAM_V, 3, 1, n_sv, st_lo2);
-  launch_grp3<8>(hi2, np, FAM_V, 3, 1, n_sv, st_hi2);
-  launch_grp3<4>(lo, np, FAM_D1, 3, 0, n_sv, st_lo);
-  launch_grp3<8>(hi, np, FAM_D1, 3, 0, n_sv, st_hi);
-  launch_grp3<4>(lo2, np, FAM_D2, 3, 0, n_sv, st_lo2);
-  launch_grp3<8>(hi2, np, FAM_D2, 3, 0, n_sv, st_hi2);
 }
 
 void launch_aggregate(const SgmArgs& a, int arith, int n_sv, cudaStream_t st) {
@@ -1254,17 +1244,34 @@ __global__ void __launch_bounds__(256) k_wta_var(WtaArgs a) {
 // pairs of neighbouring pixels are adjacent, so a warp's loads stay within a
 // few cache lines and the walk re-reads from L1.
 // variance walk + outputs of one pixel given its argmin key (value<<16 | d)
-// total of the (one or two) u16 partial sums at pair offset k
-__device__ __forceinline__ uint32_t sum_pair(const uint32_t* s, const uint32_t* s2, int k) {
-  return s2 ? __vadd2(s[k], s2[k]) : s[k];
+// the pixel's pair rows of the (1..4) u16 partial sums
+template <int N>
+struct SumRows {
+  const uint32_t* p[N];
+  __device__ __forceinline__ uint32_t operator()(int k) const {   // total at pair offset k
+    uint32_t w = p[0][k];
+#pragma unroll
+    for (int i = 1; i < N; ++i) w = __vadd2(w, p[i][k]);
+    return w;
+  }
+};
+
+template <int N>
+__device__ __forceinline__ SumRows<N> sum_rows(const WtaArgs& a, size_t off) {
+  SumRows<N> r;
+  r.p[0] = reinterpret_cast<const uint32_t*>(a.S) + off;
+#pragma unroll
+  for (int i = 1; i < N; ++i) r.p[i] = reinterpret_cast<const uint32_t*>(a.Sx[i - 1]) + off;
+  return r;
 }
 
-__device__ __forceinline__ void wta_finish(const WtaArgs& a, const uint32_t* s, const uint32_t* s2,
-                                           int lo, int hi, int j0, uint32_t best, size_t o) {
+template <int N>
+__device__ __forceinline__ void wta_finish(const WtaArgs& a, const SumRows<N>& s, int lo, int hi,
+                                           int j0, uint32_t best, size_t o) {
   const int dstar = (int)(best & 0xFFFFu);
   const uint32_t cstar = best >> 16;
   auto cell = [&](int d) -> uint32_t {
-    const uint32_t w = sum_pair(s, s2, (d >> 1) - j0);
+    const uint32_t w = s((d >> 1) - j0);
     return (d & 1) ? (w >> 16) : (w & 0xFFFFu);
   };
   long long count = 0;
@@ -1293,6 +1300,7 @@ __device__ __forceinline__ bool wta_skip(const WtaArgs& a, int svl) {
 
 constexpr int WTA_GRID = 64;   // blocks per (seq, view), grid-stride: early exits stay cheap
 
+template <int N>
 __global__ void __launch_bounds__(256) k_wta_var_u16(WtaArgs a) {
   const size_t HW = (size_t)a.W * a.H;
   const int svl = blockIdx.y;
@@ -1302,35 +1310,34 @@ __global__ void __launch_bounds__(256) k_wta_var_u16(WtaArgs a) {
     const uint2 mt = a.meta[svl * HW + pix];
     const int lo = lo_of(mt), hi = hi_of(mt);
     const int j0 = lo >> 1, j1 = hi >> 1;
-    const uint32_t* s = reinterpret_cast<const uint32_t*>(a.S) + svl * a.volcap + mt.y;
-    const uint32_t* s2 =
-        a.S2 ? reinterpret_cast<const uint32_t*>(a.S2) + svl * a.volcap + mt.y : nullptr;
+    const SumRows<N> s = sum_rows<N>(a, svl * a.volcap + mt.y);
     // key = value << 16 | d: the minimum key is the smallest value, then d
     uint32_t best = 0xFFFFFFFFu;
     {
-      const uint32_t w = sum_pair(s, s2, 0);
+      const uint32_t w = s(0);
       const uint32_t d0 = 2u * j0;
       if ((int)d0 >= lo) best = min(best, ((w & 0xFFFFu) << 16) | d0);
       if ((int)d0 + 1 <= hi) best = min(best, (w & 0xFFFF0000u) | (d0 + 1));
     }
     for (int j = j0 + 1; j < j1; ++j) {
-      const uint32_t w = sum_pair(s, s2, j - j0);
+      const uint32_t w = s(j - j0);
       const uint32_t d0 = 2u * j;
       best = min(best, min(((w & 0xFFFFu) << 16) | d0, (w & 0xFFFF0000u) | (d0 + 1)));
     }
     if (j1 > j0) {
-      const uint32_t w = sum_pair(s, s2, j1 - j0);
+      const uint32_t w = s(j1 - j0);
       const uint32_t d0 = 2u * j1;
       best = min(best, ((w & 0xFFFFu) << 16) | d0);
       if ((int)d0 + 1 <= hi) best = min(best, (w & 0xFFFF0000u) | (d0 + 1));
     }
-    wta_finish(a, s, s2, lo, hi, j0, best, svl * HW + pix);
+    wta_finish(a, s, lo, hi, j0, best, svl * HW + pix);
   }
 }
 
 // u16 sums, 8 lanes per pixel: the group streams the pixel's pairs in
 // coalesced 32-byte rows, reduces (value << 16 | d) keys with shuffles, and
 // one lane walks outward from the winner over L1-resident data.
+template <int N>
 __global__ void __launch_bounds__(256) k_wta_var_u16g(WtaArgs a) {
   const size_t HW = (size_t)a.W * a.H;
   const int lane = threadIdx.x & 31;
@@ -1344,13 +1351,11 @@ __global__ void __launch_bounds__(256) k_wta_var_u16g(WtaArgs a) {
     const uint2 mt = ok ? a.meta[svl * HW + pix] : make_uint2(0u, 0u);
     const int lo = lo_of(mt), hi = hi_of(mt);
     const int j0 = lo >> 1, j1 = hi >> 1;
-    const uint32_t* s = reinterpret_cast<const uint32_t*>(a.S) + svl * a.volcap + mt.y;
-    const uint32_t* s2 =
-        a.S2 ? reinterpret_cast<const uint32_t*>(a.S2) + svl * a.volcap + mt.y : nullptr;
+    const SumRows<N> s = sum_rows<N>(a, svl * a.volcap + mt.y);
     uint32_t best = 0xFFFFFFFFu;
     if (ok) {
       for (int j = j0 + gl; j <= j1; j += 8) {
-        const uint32_t w = sum_pair(s, s2, j - j0);
+        const uint32_t w = s(j - j0);
         const uint32_t d0 = 2u * j;
         if ((int)d0 >= lo) best = min(best, ((w & 0xFFFFu) << 16) | d0);
         if ((int)d0 + 1 <= hi) best = min(best, (w & 0xFFFF0000u) | (d0 + 1));
@@ -1358,25 +1363,31 @@ __global__ void __launch_bounds__(256) k_wta_var_u16g(WtaArgs a) {
     }
 #pragma unroll
     for (int o = 4; o; o >>= 1) best = min(best, __shfl_xor_sync(FULL, best, o));
-    if (ok && gl == 0) wta_finish(a, s, s2, lo, hi, j0, best, svl * HW + pix);
+    if (ok && gl == 0) wta_finish(a, s, lo, hi, j0, best, svl * HW + pix);
   }
 }
 
 void launch_wta_variance(const WtaArgs& a, int n_sv, cudaStream_t st) {
   const size_t HW = (size_t)a.W * a.H;
   if (a.arith == ARITH_U16 && a.dstar_in == nullptr) {
-    if (a.cells) {
-      WtaArgs lo = a, hi = a;
-      lo.select = 1;
-      hi.select = 2;
-      const unsigned g1 = (unsigned)std::min<size_t>((HW + 255) / 256, WTA_GRID);
-      const unsigned g8 = (unsigned)std::min<size_t>((HW * 8 + 255) / 256, WTA_GRID);
-      k_wta_var_u16<<<dim3(g1, n_sv), 256, 0, st>>>(lo);
-      k_wta_var_u16g<<<dim3(g8, n_sv), 256, 0, st>>>(hi);
-    } else {
-      const unsigned g1 = (unsigned)std::min<size_t>((HW + 255) / 256, WTA_GRID);
-      k_wta_var_u16<<<dim3(g1, n_sv), 256, 0, st>>>(a);
-    }
+    const int nparts = 1 + (a.Sx[0] != nullptr) + (a.Sx[1] != nullptr) + (a.Sx[2] != nullptr);
+    const unsigned g1 = (unsigned)std::min<size_t>((HW + 255) / 256, WTA_GRID);
+    const unsigned g8 = (unsigned)std::min<size_t>((HW * 8 + 255) / 256, WTA_GRID);
+    auto run = [&](auto thread_kernel, auto group_kernel) {
+      if (a.cells) {
+        WtaArgs lo = a, hi = a;
+        lo.select = 1;
+        hi.select = 2;
+        thread_kernel<<<dim3(g1, n_sv), 256, 0, st>>>(lo);
+        group_kernel<<<dim3(g8, n_sv), 256, 0, st>>>(hi);
+      } else {
+        thread_kernel<<<dim3(g1, n_sv), 256, 0, st>>>(a);
+      }
+    };
+    if (nparts == 1) run(k_wta_var_u16<1>, k_wta_var_u16g<1>);
+    else if (nparts == 2) run(k_wta_var_u16<2>, k_wta_var_u16g<2>);
+    else if (nparts == 3) run(k_wta_var_u16<3>, k_wta_var_u16g<3>);
+    else run(k_wta_var_u16<4>, k_wta_var_u16g<4>);
     return;
   }
   dim3 grid((unsigned)((HW + 7) / 8), n_sv);
@@ -1388,7 +1399,8 @@ void launch_wta_variance(const WtaArgs& a, int n_sv, cudaStream_t st) {
 
 __global__ void k_export_dense(const uint2* __restrict__ meta, const void* __restrict__ vol,
                                int vol_f32, int W, int H, int D, float* __restrict__ out,
-                               const void* __restrict__ vol2) {
+                               const void* __restrict__ vol2, const void* __restrict__ vol3,
+                               const void* __restrict__ vol4) {
   const size_t HW = (size_t)W * H;
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= HW * D) return;
@@ -1405,6 +1417,8 @@ __global__ void k_export_dense(const uint2* __restrict__ meta, const void* __res
     } else {
       uint32_t w = reinterpret_cast<const uint32_t*>(vol)[k];
       if (vol2) w = __vadd2(w, reinterpret_cast<const uint32_t*>(vol2)[k]);
+      if (vol3) w = __vadd2(w, reinterpret_cast<const uint32_t*>(vol3)[k]);
+      if (vol4) w = __vadd2(w, reinterpret_cast<const uint32_t*>(vol4)[k]);
       const uint32_t h = (d & 1) ? (w >> 16) : (w & 0xFFFFu);
       // u16 costs use 0x8000 as +inf; u16 sums are always finite in-interval
       v = (vol_f32 == EXPORT_U16_COST && h >= INF16) ? INFINITY : (float)h;
@@ -1414,10 +1428,11 @@ __global__ void k_export_dense(const uint2* __restrict__ meta, const void* __res
 }
 
 void launch_export_dense(const uint2* meta, const void* vol, int vol_f32, int W, int H, int d_max,
-                         float* out, cudaStream_t st, const void* vol2) {
+                         float* out, cudaStream_t st, const void* vol2, const void* vol3,
+                         const void* vol4) {
   const size_t n = (size_t)W * H * (d_max + 1);
   k_export_dense<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(meta, vol, vol_f32, W, H, d_max + 1,
-                                                               out, vol2);
+                                                               out, vol2, vol3, vol4);
 }
 
 // dense (H, W, D) float32 -> ragged pairs (u16 when as_f32 == 0)

@@ -1,0 +1,61 @@
+"""The benchmark's own code path against the oracle: BatchedPipeline with
+device-resident inputs and deferred (non-syncing) steps, B = 12 sequences
+(> 8, so two concurrent partial sums as in the B = 64 bench), the device
+renderer's scenes, both SGM regime kernels (frame 0 full range, later
+frames reduced)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def test_batched_deferred_path_matches_oracle():
+    import torch
+    from paper_1708_06301_b200 import _lib, pipeline, scenes
+    from paper_1708_06301_b200.core import StereoRig
+    B, n = 12, 4
+    rig = StereoRig(f=180.0, b=0.54, cx=151.0, cy=46.0, width=310, height=94, d_max=40)
+    specs = [scenes.sequence_spec(seed=900 + s, n_frames=n, step=0.5, z_range=(4.0, 30.0))
+             for s in range(B)]
+    rs = _lib.rig_struct(rig)
+    boxes = np.ascontiguousarray(np.stack([sp[0] for sp in specs]), np.float64)
+    seeds = np.arange(B, dtype=np.int64) + 3
+    imgs = torch.empty((n, B, 2, rig.height, rig.width), dtype=torch.uint8, device="cuda")
+    for k in range(n):
+        poses = np.ascontiguousarray(np.stack([sp[1][k] for sp in specs]), np.float64)
+        _lib.call("es_render", ctypes.byref(rs), _lib.ptr(boxes), boxes.shape[1], _lib.ptr(poses),
+                  _lib.ptr(seeds), B, ctypes.c_double(0.05), 12,
+                  ctypes.c_void_p(imgs[k].data_ptr()), None, ctypes.c_void_p(0))
+    torch.cuda.synchronize()
+    host = imgs.cpu().numpy()
+    bp = pipeline.BatchedPipeline(rig, B)
+    # frame 0 synced (establishes have_state), the rest deferred like the bench
+    bp.process_frames(None, [sp[2][0] for sp in specs], sync=True, images_dev=imgs[0].data_ptr())
+    for k in range(1, n):
+        bp.process_frames(None, [sp[2][k] for sp in specs], sync=False,
+                          images_dev=imgs[k].data_ptr())
+    bp.sync()
+    kitti = bp.fused_kitti(0)
+    for s in range(B):
+        orc = O.OracleStereo(rig.f, rig.b, rig.cx, rig.cy, rig.width, rig.height, rig.d_max)
+        for k in range(n):
+            want = orc.step(host[k, s, 0], host[k, s, 1], specs[s][2][k])
+        got = bp.result(s)
+        for view, name in ((0, "left"), (1, "right")):
+            meas = got.measured_left if view == 0 else got.measured_right
+            assert np.array_equal(meas.values, want[name + "_meas"][0]), (s, name)
+            fd = got.fused.left if view == 0 else got.fused.right
+            fp = got.fused.left_var if view == 0 else got.fused.right_var
+            assert np.array_equal(fd.valid, want[name + "_fused"][2]), (s, name)
+            np.testing.assert_allclose(fd.values, want[name + "_fused"][0], rtol=1e-9, atol=0)
+            np.testing.assert_allclose(fp.values, want[name + "_fused"][1], rtol=1e-9, atol=0)
+        # the e2e result encoding (kitti_io.write_disparity_png)
+        fl = want["left_fused"]
+        enc = np.where(fl[2], np.maximum(np.rint(fl[0] * 256.0), 1.0), 0.0).astype(np.uint16)
+        assert np.array_equal(kitti[s], enc), s
+        assert got.search_fraction_left < 1.0

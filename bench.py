@@ -39,20 +39,45 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-H, W, D_MAX = 375, 1242, 127
-RIG = dict(f=718.9, b=0.54, cx=607.0, cy=185.0, width=W, height=H, d_max=D_MAX)
-SEQ_FRAMES = 50
+# BASELINE.json configs this bench runs (5: the headline; 4: the high-resolution
+# variant, batched the same way)
+CONFIGS = {
+    5: dict(H=375, W=1242, d_max=127, f=718.9, b=0.54, cx=607.0, cy=185.0, frames=50,
+            step=1.0, yaw_deg=0.5, batch=64,
+            workload="config5: B independent 1242x375 sequences per GPU, D=128, "
+                     "8 paths, predicted frames (frame 0 full range in warm-up)"),
+    4: dict(H=1024, W=2048, d_max=255, f=1400.0, b=0.3, cx=1023.5, cy=511.5, frames=30,
+            step=1.5, yaw_deg=1.0, batch=8,
+            workload="config4: B independent 2048x1024 sequences per GPU, D=256, "
+                     "8 paths, 1.5 m/frame, yaw N(0,1 deg), predicted frames "
+                     "(frame 0 full range in warm-up)"),
+}
+CFG = CONFIGS[5]
+H, W, D_MAX = CFG["H"], CFG["W"], CFG["d_max"]
+RIG = dict(f=CFG["f"], b=CFG["b"], cx=CFG["cx"], cy=CFG["cy"], width=W, height=H, d_max=D_MAX)
+SEQ_FRAMES = CFG["frames"]
+
+
+def use_config(n):
+    g = globals()
+    c = CONFIGS[n]
+    g["CFG"] = c
+    g["H"], g["W"], g["D_MAX"] = c["H"], c["W"], c["d_max"]
+    g["RIG"] = dict(f=c["f"], b=c["b"], cx=c["cx"], cy=c["cy"], width=c["W"], height=c["H"],
+                    d_max=c["d_max"])
+    g["SEQ_FRAMES"] = c["frames"]
 TEXTURE_SCALE = 0.05
 KERNELS_PER_STEP = 15   # zmax, zidx, fill_h, fill_v, cost, 4 families x 2 sgm variants, wta, fuse
 
 
-def measured_traffic(batch, texture_scale):
+def measured_traffic(config, batch, texture_scale):
     """DRAM bytes per step of the aggregation stage from the committed ncu
     capture of the same workload (profiles/r01/agg_traffic.json), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "r01", "agg_traffic.json")) as fh:
             t = json.load(fh)
-        if t["batch"] == batch and abs(t["texture_scale"] - texture_scale) < 1e-12:
+        if (t.get("config", 5) == config and t["batch"] == batch
+                and abs(t["texture_scale"] - texture_scale) < 1e-12):
             return float(t["dram_bytes_per_step"])
     except Exception:
         pass
@@ -72,7 +97,8 @@ def peaks():
 
 def sequence_specs(n, seed0):
     from paper_1708_06301_b200 import scenes
-    return [scenes.sequence_spec(seed=seed0 + s, n_frames=SEQ_FRAMES) for s in range(n)]
+    return [scenes.sequence_spec(seed=seed0 + s, n_frames=SEQ_FRAMES, step=CFG["step"],
+                                 yaw_deg=CFG["yaw_deg"]) for s in range(n)]
 
 
 def render_frames(specs, frames, device):
@@ -143,9 +169,11 @@ class Clocks:
 # ----------------------------------------------------------------- CPU port
 
 def _cpu_worker(args):
-    left0, right0, left1, right1, motion = args
+    # spawned: the module globals are config 5's, so the rig travels with the job
+    left0, right0, left1, right1, motion, rig = args
     import oracle as O
-    orc = O.OracleStereo(RIG["f"], RIG["b"], RIG["cx"], RIG["cy"], W, H, D_MAX)
+    orc = O.OracleStereo(rig["f"], rig["b"], rig["cx"], rig["cy"], rig["width"], rig["height"],
+                         rig["d_max"])
     orc.step(left0, right0, None)
     t0 = time.perf_counter()
     orc.step(left1, right1, motion)
@@ -156,14 +184,15 @@ def cpu_baseline(imgs0, imgs1, motions, procs):
     """numpy oracle port: P processes, each one full-range warm frame (not
     timed) then one timed predicted frame of its own sequence."""
     P = min(procs, len(motions))
-    jobs = [(imgs0[s, 0], imgs0[s, 1], imgs1[s, 0], imgs1[s, 1], motions[s]) for s in range(P)]
+    jobs = [(imgs0[s, 0], imgs0[s, 1], imgs1[s, 0], imgs1[s, 1], motions[s], RIG)
+            for s in range(P)]
     t0 = time.perf_counter()
     with mp.get_context("spawn").Pool(P) as pool:
         per = pool.map(_cpu_worker, jobs)
     wall = time.perf_counter() - t0
     fps = P / max(per)
     return {"value": fps, "unit": "frames/s", "cores": P, "kind": "port",
-            "sample": f"{P} sequences x 1 predicted frame (1242x375, D=128) in {P} parallel "
+            "sample": f"{P} sequences x 1 predicted frame ({W}x{H}, D={D_MAX + 1}) in {P} parallel "
                       f"processes; per-frame {min(per):.1f}-{max(per):.1f} s; wall {wall:.0f} s "
                       "incl. the untimed full-range frame"}
 
@@ -175,7 +204,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=64, help="sequences per GPU (config 5: 64)")
+    ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS),
+                    help="BASELINE.json config: 5 (headline, 1242x375 D=128) or 4 "
+                         "(2048x1024 D=256)")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="sequences per GPU (default: config 5: 64, config 4: 8)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-procs", type=int, default=min(8, os.cpu_count() or 1))
     ap.add_argument("--no-cpu", action="store_true")
@@ -185,6 +218,12 @@ def main():
                          "search fractions, 0.2 gives ~10%%")
     args = ap.parse_args()
     globals()["TEXTURE_SCALE"] = args.texture_scale
+    use_config(args.config)
+    if args.batch is None:
+        args.batch = CFG["batch"]
+    if args.config == 4:
+        # a 2048x1024 D=256 numpy frame needs several GB and minutes per process
+        args.cpu_procs = min(args.cpu_procs, 2)
 
     from paper_1708_06301_b200 import sharding
     rank, world, local = sharding.world()
@@ -198,8 +237,7 @@ def main():
     K, Wm, B = args.steps, max(args.warmup, 3), args.batch
     if Wm + K > SEQ_FRAMES:
         raise SystemExit(f"warmup + steps must be <= {SEQ_FRAMES} (sequence length)")
-    config = {"workload": "config5: B independent 1242x375 sequences per GPU, D=128, "
-                          "8 paths, predicted frames (frame 0 full range in warm-up)",
+    config = {"workload": CFG["workload"],
               "batch_per_gpu": B, "height": H, "width": W, "d_max": D_MAX,
               "l2": "working set per step (ragged volumes of all sequences) >> 126 MB L2"}
 
@@ -319,7 +357,7 @@ def main():
                      "frac": achieved / peak,
                      # ncu DRAM bytes of the same stage per step (committed capture of
                      # this workload), vs bytes_per_step algorithmic
-                     "traffic": measured_traffic(B, TEXTURE_SCALE),
+                     "traffic": measured_traffic(args.config, B, TEXTURE_SCALE),
                      "traffic_unit": "bytes per step (all sequences, both views)",
                      "peak_kind": peak_kind, "bytes_per_step": agg_bytes},
         "pipeline_roofline": {"achieved": frame_bytes / (ms_max / K / 1e3) / 1e9,

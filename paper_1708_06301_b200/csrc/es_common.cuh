@@ -44,9 +44,12 @@ __host__ __device__ inline int npairs_max(int d_max) { return (d_max >> 1) + 1; 
 // allocation of pixel_slots() pairs at an even offset o, so (offset - j0) is
 // even and the two pairs 2k, 2k+1 any lane holds form one aligned 8-byte word
 // inside the pixel's own allocation.
+// Padding slots (before / after the interval pairs) are written +inf by the
+// cost pass, so aligned accesses that overlap them read +inf.
+__host__ __device__ inline uint32_t pad_before(int lo) { return ((uint32_t)lo >> 1) & 1u; }
 __host__ __device__ inline uint32_t pixel_slots(int lo, int hi) {
   const uint32_t j0 = (uint32_t)lo >> 1, j1 = (uint32_t)hi >> 1;
-  return (j1 - j0 + 1 + (j0 & 1) + 1) & ~1u;
+  return (j1 - j0 + 1 + pad_before(lo) + 1) & ~1u;
 }
 // pairs reserved per image row (multiple of 4 so rows start 16-byte aligned)
 __host__ __device__ inline size_t row_capacity(int W, int d_max) {

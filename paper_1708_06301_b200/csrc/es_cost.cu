@@ -61,8 +61,11 @@ __global__ void __launch_bounds__(COST_NT) k_cost(CostArgs a) {
     rowlh[x] = m.x;
   }
   __syncthreads();
+  // the row's slots up to the end of the last pixel's allocation (its
+  // trailing padding slot included: padding holds +inf)
   const uint32_t last = rowlh[W - 1];
-  const uint32_t row_pairs = rowoff[W - 1] + ((last >> 16) >> 1) - ((last & 0xFFFFu) >> 1) + 1;
+  const uint32_t row_pairs = rowoff[W - 1] - pad_before(last & 0xFFFFu) +
+                             pixel_slots(last & 0xFFFFu, last >> 16);
   const uint32_t border = (uint32_t)(a.window * a.window * 255);
   uint32_t* C = a.C + (size_t)svl * a.volcap + rowbase;
   const int sign = view == 0 ? -1 : 1;
@@ -135,8 +138,11 @@ __global__ void __launch_bounds__(COST_NT) k_cost_w3(CostArgs a) {
     rowlh[x] = m.x;
   }
   __syncthreads();
+  // the row's slots up to the end of the last pixel's allocation (its
+  // trailing padding slot included: padding holds +inf)
   const uint32_t last = rowlh[W - 1];
-  const uint32_t row_pairs = rowoff[W - 1] + ((last >> 16) >> 1) - ((last & 0xFFFFu) >> 1) + 1;
+  const uint32_t row_pairs = rowoff[W - 1] - pad_before(last & 0xFFFFu) +
+                             pixel_slots(last & 0xFFFFu, last >> 16);
   if (threadIdx.x == 0) rowoff[W] = row_pairs;
   __syncthreads();
   const uint32_t border = 9u * 255u;
@@ -209,8 +215,9 @@ __global__ void __launch_bounds__(COST_NT) k_cost_w3(CostArgs a) {
       // off-image centres take the border cost; cells outside [lo, hi] are +inf
       if ((unsigned)(x + sign * d0) > (unsigned)(W - 1)) c0 = border;
       if ((unsigned)(x + sign * (d0 + 1)) > (unsigned)(W - 1)) c1 = border;
-      if (d0 < lo) c0 = INF16;
-      if (d0 + 1 > hi) c1 = INF16;
+      // (padding slots lie wholly outside [lo, hi])
+      if (d0 < lo || d0 > hi) c0 = INF16;
+      if (d0 + 1 < lo || d0 + 1 > hi) c1 = INF16;
       out[r] = c0 | (c1 << 16);
     }
     if (q0 + COST_R <= row_pairs && ((rowbase + q0) & 3u) == 0 && ((a.volcap * svl) & 3u) == 0) {

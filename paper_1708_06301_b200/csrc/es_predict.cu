@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(NT) k_fill_v_intervals(PredArgs a) {
     const size_t i = sv * HW + (size_t)y * W + x;
     const uint32_t m = a.meta[i].x;
     const int lo = m & 0xFFFFu, hi = m >> 16;
-    a.meta[i].y = rowbase + base + ((uint32_t)(lo >> 1) & 1u);
+    a.meta[i].y = rowbase + base + pad_before(lo);
     base += pixel_slots(lo, hi);
   }
   atomicAdd(&cells_smem, my_cells);
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(NT) k_meta_from_intervals(const int64_t* __res
     const size_t i = (size_t)y * W + x;
     const uint32_t m = meta[i].x;
     const int lo = m & 0xFFFFu, hi = m >> 16;
-    meta[i].y = rowbase + base + ((uint32_t)(lo >> 1) & 1u);
+    meta[i].y = rowbase + base + pad_before(lo);
     base += pixel_slots(lo, hi);
   }
 }

@@ -281,8 +281,10 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp(SgmArgs a, int fam, 
   uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
   // keep the per-(seq, view) bases in registers (ptxas otherwise re-derives
   // them from the parameter bank at every load and store)
+#ifndef ES_GRP3_NOPIN
   asm volatile("" : "+l"(C));
   asm volatile("" : "+l"(S));
+#endif
   const uint32_t p1x2 = a.p1i * 0x10001u;
   const uint32_t p2 = a.p2i;
   const int len = fam == FAM_H ? W : H;
@@ -440,8 +442,10 @@ __global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp2(SgmArgs a, int fam,
   const uint32_t* __restrict__ C =
       reinterpret_cast<const uint32_t*>(a.C) + (size_t)blockIdx.y * a.volcap;
   uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
+#ifndef ES_GRP3_NOPIN
   asm volatile("" : "+l"(C));
   asm volatile("" : "+l"(S));
+#endif
   const uint32_t p1x2 = a.p1i * 0x10001u;
   const uint32_t p2 = a.p2i;
   const int len = fam == FAM_H ? W : H;
@@ -670,6 +674,12 @@ __global__ void __launch_bounds__(GRP_WARPS * 32, (G == 4 ? 4 : 1)) k_sgm_grp3(S
   const uint32_t* __restrict__ C =
       reinterpret_cast<const uint32_t*>(a.C) + (size_t)blockIdx.y * a.volcap;
   uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
+  // keep the per-view bases in registers: one IMAD.WIDE per access instead of
+  // re-deriving blockIdx.y * volcap under register pressure
+#ifndef ES_GRP3_NOPIN
+  asm volatile("" : "+l"(C));
+  asm volatile("" : "+l"(S));
+#endif
   const uint32_t p1x2 = a.p1i * 0x10001u;
   const uint32_t p2 = a.p2i;
   const int len = fam == FAM_H ? W : H;
@@ -781,8 +791,14 @@ __global__ void __launch_bounds__(GRP_WARPS * 32, (G == 4 ? 4 : 1)) k_sgm_grp3(S
           const uint32_t cb = __vminu2(__viaddmin_u16x2(nbb, p1x2, pb), mp2);
           const uint32_t rel = (uint32_t)(c * CW + 2 * gl - cur.j0);
 #ifndef ES_GRP3_SCALAR
-          const uint32_t cwa = rel < cur.span ? cn[2 * c] : INF16x2;       // mask at use
+          // no mask: the out-of-interval pair of a word is the pixel's own
+          // padding slot, which the cost pass fills with +inf (es_common.cuh)
+#ifdef ES_GRP3_MASK
+          const uint32_t cwa = rel < cur.span ? cn[2 * c] : INF16x2;
           const uint32_t cwb = rel + 1 < cur.span ? cn[2 * c + 1] : INF16x2;
+#else
+          const uint32_t cwa = cn[2 * c], cwb = cn[2 * c + 1];
+#endif
 #else
           const uint32_t cwa = cn[2 * c], cwb = cn[2 * c + 1];
 #endif
@@ -1130,8 +1146,21 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
     lo.S = S[p];
     hi.S = S[p];
     const int init = k < parts;   // first family into this partial sum
-    launch_grp3<4>(lo, np, fams[k], 3, init, n_sv, st_lo[p]);
-    launch_grp3<8>(hi, np, fams[k], 3, init, n_sv, st_hi[p]);
+    // lanes per chain: reduced intervals 4 lanes while the full range fits
+    // 8 chunks of 2G pairs (D <= 128), wide ones twice that; larger D widens
+    // both so the register-resident chunk arrays never exceed 8 (16 for the
+    // widest instance) -- at NCH 16 the 4-lane instance spills (measured,
+    // config 4: D = 256)
+    if (np <= 64) {
+      launch_grp3<4>(lo, np, fams[k], 3, init, n_sv, st_lo[p]);
+      launch_grp3<8>(hi, np, fams[k], 3, init, n_sv, st_hi[p]);
+    } else if (np <= 128) {
+      launch_grp3<8>(lo, np, fams[k], 3, init, n_sv, st_lo[p]);
+      launch_grp3<16>(hi, np, fams[k], 3, init, n_sv, st_hi[p]);
+    } else {
+      launch_grp3<16>(lo, np, fams[k], 3, init, n_sv, st_lo[p]);
+      launch_grp3<32>(hi, np, fams[k], 3, init, n_sv, st_hi[p]);
+    }
   }
 }
 
@@ -1371,8 +1400,11 @@ void launch_wta_variance(const WtaArgs& a, int n_sv, cudaStream_t st) {
   const size_t HW = (size_t)a.W * a.H;
   if (a.arith == ARITH_U16 && a.dstar_in == nullptr) {
     const int nparts = 1 + (a.Sx[0] != nullptr) + (a.Sx[1] != nullptr) + (a.Sx[2] != nullptr);
-    const unsigned g1 = (unsigned)std::min<size_t>((HW + 255) / 256, WTA_GRID);
-    const unsigned g8 = (unsigned)std::min<size_t>((HW * 8 + 255) / 256, WTA_GRID);
+    // blocks per (seq, view): WTA_GRID, or enough that few large views still
+    // fill every SM (config 4: 16 views of 2048x1024)
+    const size_t per_sv = std::max<size_t>(WTA_GRID, (148 * 16 + n_sv - 1) / n_sv);
+    const unsigned g1 = (unsigned)std::min<size_t>((HW + 255) / 256, per_sv);
+    const unsigned g8 = (unsigned)std::min<size_t>((HW * 8 + 255) / 256, per_sv);
     auto run = [&](auto thread_kernel, auto group_kernel) {
       if (a.cells) {
         WtaArgs lo = a, hi = a;
@@ -1442,6 +1474,15 @@ __global__ void k_import_dense(const float* __restrict__ dense, const uint2* __r
   if (pix >= (size_t)W * H) return;
   const uint2 mt = meta[pix];
   const int lo = lo_of(mt), hi = hi_of(mt);
+  // the pixel's padding slots hold +inf too (read by the aggregation's
+  // aligned multi-pair accesses, es_common.cuh)
+  const uint32_t a0 = mt.y - pad_before(lo), a1 = a0 + pixel_slots(lo, hi);
+  const uint32_t k0 = mt.y, k1 = mt.y + (uint32_t)((hi >> 1) - (lo >> 1) + 1);
+  for (uint32_t k = a0; k < a1; ++k) {
+    if (k >= k0 && k < k1) continue;
+    if (as_f32) reinterpret_cast<float2*>(vol)[k] = make_float2(INFINITY, INFINITY);
+    else reinterpret_cast<uint32_t*>(vol)[k] = INF16x2;
+  }
   for (int j = lo >> 1; j <= (hi >> 1); ++j) {
     const size_t k = (size_t)mt.y + (size_t)(j - (lo >> 1));
     float v[2];

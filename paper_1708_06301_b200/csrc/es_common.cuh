@@ -40,21 +40,23 @@ constexpr int ERR_NONPOSITIVE_D = 2;
 
 __host__ __device__ inline int npairs_max(int d_max) { return (d_max >> 1) + 1; }
 
-// Storage of one pixel: its pairs start at an offset o + (j0 & 1) inside an
-// allocation of pixel_slots() pairs at an even offset o, so (offset - j0) is
-// even and the two pairs 2k, 2k+1 any lane holds form one aligned 8-byte word
-// inside the pixel's own allocation.
+// Storage of one pixel: its pairs start at an offset o + (j0 & 3) inside an
+// allocation of pixel_slots() pairs at an offset o that is a multiple of 4,
+// so (offset - j0) is a multiple of 4: the 8-cell block b (cells 8b .. 8b+7,
+// pairs 4b .. 4b+3) of any pixel is one aligned 16-byte word inside the
+// pixel's own allocation, and the pairs 2k, 2k+1 one aligned 8-byte word.
 // Padding slots (before / after the interval pairs) are written +inf by the
 // cost pass, so aligned accesses that overlap them read +inf.
-__host__ __device__ inline uint32_t pad_before(int lo) { return ((uint32_t)lo >> 1) & 1u; }
+__host__ __device__ inline uint32_t pad_before(int lo) { return ((uint32_t)lo >> 1) & 3u; }
 __host__ __device__ inline uint32_t pixel_slots(int lo, int hi) {
   const uint32_t j0 = (uint32_t)lo >> 1, j1 = (uint32_t)hi >> 1;
-  return (j1 - j0 + 1 + pad_before(lo) + 1) & ~1u;
+  return (j1 - j0 + 1 + pad_before(lo) + 3) & ~3u;
 }
-// pairs reserved per image row (multiple of 4 so rows start 16-byte aligned)
+// pairs reserved per image row (a multiple of 4: rows start 16-byte aligned);
+// a pixel never needs more than the full range rounded up to 4 pairs
 __host__ __device__ inline size_t row_capacity(int W, int d_max) {
-  const size_t per = (size_t)((npairs_max(d_max) + 1) & ~1);
-  return ((size_t)W * per + 3) & ~(size_t)3;
+  const size_t per = (size_t)((npairs_max(d_max) + 3) & ~3);
+  return (size_t)W * per;
 }
 
 __device__ __forceinline__ uint32_t lo_of(uint2 m) { return m.x & 0xFFFFu; }

@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(NT) k_fill_v_intervals(PredArgs a) {
   }
   uint32_t total;
   uint32_t base = block_exclusive_scan<NT>(my_pairs, scan_smem, total);
-  // pass 2: offsets (first pair at an even slot offset + (j0 & 1))
+  // pass 2: offsets (first pair at a 4-aligned slot offset + (j0 & 3))
   const uint32_t rowbase = (uint32_t)(y * row_capacity(W, d_max));
   for (int x = x0; x < x1; ++x) {
     const size_t i = sv * HW + (size_t)y * W + x;

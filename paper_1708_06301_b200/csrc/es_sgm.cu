@@ -859,6 +859,240 @@ static void launch_grp3(const SgmArgs& a, int nch_pairs, int fam, int sweeps, in
   else go(k_sgm_grp3<G, 16>);
 }
 
+// ------------------------------------------------------------ grouped, PPL pairs/lane
+//
+// The production u16 kernel.  As k_sgm_grp3 (a warp walks 32/G chains in
+// lockstep, G lanes per chain, absolute chunks, union-of-chunks loop, operands
+// fetched two steps ahead into alternating register sets) with the per-chunk
+// overhead cut down:
+//  * every lane owns PPL consecutive pairs (2*PPL cells) of a chunk, one
+//    aligned 8- or 16-byte word of the pixel's allocation (pixel_slots keeps
+//    (offset - j0) a multiple of 4), so one load / store serves them all;
+//  * per step each lane forms one signed base offset; chunk c's operands are
+//    at base + c*CW, an immediate offset, and one compare gives the chunk's
+//    predicate;
+//  * no select for a chain's first pixel: a chain that is inactive holds
+//    +inf-ish values (>= 0x8000) and mp2 = ng = 0x8000, so its first active
+//    pixel computes min(...) = 0x8000 and L = C + 0x8000 + 0x8000 = C;
+//  * no select for the first family's forward sweep: the predicated partial
+//    sum load leaves 0.
+constexpr int G4_WARPS = 4;
+
+struct G4Step {
+  int base;         // pair offset (this view) of the lane's pairs in chunk 0
+  int relb;         // PPL*gl - j0 + PPL - 1: chunk c has a pair in [j0, j1] iff
+  uint32_t spanp;   //   (unsigned)(relb + c*CW) < spanp = span + PPL - 1
+  uint32_t um;      // warp-uniform chunk mask (union over the warp's chains)
+};
+
+template <int PPL>
+struct Vec;
+template <>
+struct Vec<2> {
+  __device__ static __forceinline__ void ldc(const uint32_t* p, bool pred, uint32_t* o) {
+    uint32_t a = INF16x2, b = INF16x2;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q ld.global.nc.v2.u32 {%0, %1}, [%2];\n\t}\n"
+                 : "+r"(a), "+r"(b) : "l"(p), "r"((int)pred));
+    o[0] = a; o[1] = b;
+  }
+  __device__ static __forceinline__ void ld(const uint32_t* p, bool pred, uint32_t* o) {
+    uint32_t a = 0u, b = 0u;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q ld.global.v2.u32 {%0, %1}, [%2];\n\t}\n"
+                 : "+r"(a), "+r"(b) : "l"(p), "r"((int)pred));
+    o[0] = a; o[1] = b;
+  }
+  __device__ static __forceinline__ void st(uint32_t* p, bool pred, const uint32_t* v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q st.global.v2.u32 [%0], {%1, %2};\n\t}\n"
+                 :: "l"(p), "r"(v[0]), "r"(v[1]), "r"((int)pred) : "memory");
+  }
+};
+template <>
+struct Vec<4> {
+  __device__ static __forceinline__ void ldc(const uint32_t* p, bool pred, uint32_t* o) {
+    uint32_t a = INF16x2, b = INF16x2, c = INF16x2, d = INF16x2;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}\n"
+                 : "+r"(a), "+r"(b), "+r"(c), "+r"(d) : "l"(p), "r"((int)pred));
+    o[0] = a; o[1] = b; o[2] = c; o[3] = d;
+  }
+  __device__ static __forceinline__ void ld(const uint32_t* p, bool pred, uint32_t* o) {
+    uint32_t a = 0u, b = 0u, c = 0u, d = 0u;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}\n"
+                 : "+r"(a), "+r"(b), "+r"(c), "+r"(d) : "l"(p), "r"((int)pred));
+    o[0] = a; o[1] = b; o[2] = c; o[3] = d;
+  }
+  __device__ static __forceinline__ void st(uint32_t* p, bool pred, const uint32_t* v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.global.v4.u32 [%0], {%1, %2, %3, %4};\n\t}\n"
+                 :: "l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"((int)pred) : "memory");
+  }
+};
+
+template <int G, int NCH, int PPL, int MINB>
+__global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int fam, int init) {
+  constexpr int NG = 32 / G;
+  constexpr int CW = PPL * G;      // pairs per chunk
+  constexpr int NW = PPL * NCH;    // words per lane
+  constexpr uint32_t NONE = 0xFFFFFFFFu;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int grp = lane / G;
+  const int gbase = lane & ~(G - 1);
+  const int W = a.W, H = a.H;
+  const int nchains = fam == FAM_H ? H : (fam == FAM_V ? W : W + H - 1);
+  const int c0 = (blockIdx.x * G4_WARPS + (threadIdx.x >> 5)) * NG;
+  if (c0 >= nchains) return;
+  if (a.select) {
+    const double frac = (double)a.cells[blockIdx.y] / ((double)W * H * (a.d_max + 1));
+    if ((a.select == 1) == (frac > a.split)) return;
+  }
+  const int ch = c0 + grp;
+  const size_t HW = (size_t)W * H;
+  const uint2* __restrict__ meta = a.meta + (size_t)blockIdx.y * HW;
+  const uint32_t* __restrict__ C =
+      reinterpret_cast<const uint32_t*>(a.C) + (size_t)blockIdx.y * a.volcap;
+  uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
+  asm volatile("" : "+l"(C));
+  asm volatile("" : "+l"(S));
+  const int len = fam == FAM_H ? W : H;
+  const int src_l = gbase | ((gl + G - 1) & (G - 1));
+  const int src_r = gbase | ((gl + 1) & (G - 1));
+  auto umask = [](int lo, int hi) -> uint32_t {
+    return hi < lo ? 0u : ((hi >= 31 ? 0xFFFFFFFFu : ((2u << hi) - 1u)) & ~((1u << lo) - 1u));
+  };
+  for (int bwd = 0; bwd < 2; ++bwd) {
+    const bool load_sum = !(init && bwd == 0);
+    auto load_meta = [&](int tb) -> uint2 {
+      int x, y;
+      const int t = tb + gl;
+      if (t < len && grp_pixel(fam, bwd, ch, t, W, H, x, y)) return meta[(size_t)y * W + x];
+      return make_uint2(NONE, 0u);
+    };
+    uint2 mb_cur = load_meta(0);
+    uint2 mb_next = load_meta(G);
+    uint2 mb_next2 = load_meta(2 * G);
+    int tb = 0;
+    auto info = [&](int tp) -> G4Step {
+      G4Step s{0, 0, 0u, 0u};
+      int clo = NCH, chi = -1;
+      if (tp < len) {
+        if (tp == tb + G) {
+          tb += G;
+          mb_cur = mb_next;
+          mb_next = mb_next2;
+          mb_next2 = load_meta(tb + 2 * G);
+        }
+        const int r = tp - tb;
+        const uint32_t mx = __shfl_sync(FULL, mb_cur.x, gbase | r);
+        const uint32_t my = __shfl_sync(FULL, mb_cur.y, gbase | r);
+        if (mx != NONE) {
+          const int j0 = (int)((mx & 0xFFFFu) >> 1);
+          const int j1 = (int)((mx >> 16) >> 1);
+          s.base = (int)(my - (uint32_t)j0) + PPL * gl;
+          s.relb = PPL * gl - j0 + PPL - 1;
+          s.spanp = (uint32_t)(j1 - j0 + PPL);
+          clo = j0 / CW;
+          chi = j1 / CW;
+        }
+      }
+      s.um = umask(__reduce_min_sync(FULL, clo), __reduce_max_sync(FULL, chi));
+      return s;
+    };
+    auto pred_of = [&](const G4Step& s, int c) -> bool {
+      return (uint32_t)(s.relb + c * CW) < s.spanp;
+    };
+    auto fetch = [&](const G4Step& s, uint32_t (&cn)[NW], uint32_t (&sn)[NW], int c) {
+      const bool p = pred_of(s, c);
+      Vec<PPL>::ldc(C + s.base + c * CW, p, &cn[c * PPL]);
+      Vec<PPL>::ld(S + s.base + c * CW, p && load_sum, &sn[c * PPL]);
+    };
+    uint32_t prev[NW], cA[NW], sA[NW], cB[NW], sB[NW];
+    G4Step s0 = info(0);
+    G4Step s1 = info(1);
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+#pragma unroll
+      for (int k = 0; k < PPL; ++k) prev[c * PPL + k] = INF16x2;
+      fetch(s0, cA, sA, c);
+      fetch(s1, cB, sB, c);
+    }
+    uint32_t mp2 = INF16x2, ng = INF16x2;   // no predecessor: L = C
+    const uint32_t p1x2 = a.p1i * 0x10001u;
+    auto step = [&](const G4Step& cur, const G4Step& nn, uint32_t (&cn)[NW], uint32_t (&sn)[NW]) {
+      uint32_t nmin = INF16x2;
+      uint32_t left_old = INF16x2;   // previous chunk's last word, before overwrite
+      uint32_t* Sb = S + cur.base;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        uint32_t P[PPL];
+#pragma unroll
+        for (int k = 0; k < PPL; ++k) P[k] = prev[c * PPL + k];
+        if ((cur.um >> c) & 1u) {
+          const uint32_t srcl = gl == G - 1 ? left_old : P[PPL - 1];
+          const uint32_t srcr = gl == 0 ? (c + 1 < NCH ? prev[(c + 1 < NCH ? c + 1 : 0) * PPL] : INF16x2) : P[0];
+          const uint32_t pl = __shfl_sync(FULL, srcl, src_l);
+          const uint32_t pr = __shfl_sync(FULL, srcr, src_r);
+          uint32_t X[PPL + 1];
+          X[0] = __byte_perm(pl, P[0], 0x5432);
+#pragma unroll
+          for (int k = 1; k < PPL; ++k) X[k] = __byte_perm(P[k - 1], P[k], 0x5432);
+          X[PPL] = __byte_perm(P[PPL - 1], pr, 0x5432);
+          uint32_t L[PPL], Ssum[PPL];
+#pragma unroll
+          for (int k = 0; k < PPL; ++k) {
+            // L = C + min(Lp(d), Lp(d-1)+P1, Lp(d+1)+P1, m+P2) - m   (sgm.py:205-215)
+            const uint32_t cand = __viaddmin_u16x2(__vminu2(X[k], X[k + 1]), p1x2, __vminu2(P[k], mp2));
+            L[k] = __vadd2(cn[c * PPL + k], __vadd2(cand, ng));
+            Ssum[k] = __vadd2(sn[c * PPL + k], L[k]);
+            prev[c * PPL + k] = L[k];
+          }
+          if (PPL == 4) {
+            nmin = __vimin3_u16x2(nmin, L[0], L[1]);
+            nmin = __vimin3_u16x2(nmin, L[PPL - 2], L[PPL - 1]);
+          } else {
+            nmin = __vimin3_u16x2(nmin, L[0], L[PPL - 1]);
+          }
+          // halves outside [lo, hi] land in the pixel's own padding /
+          // out-of-interval slots, which nothing reads
+          Vec<PPL>::st(Sb + c * CW, pred_of(cur, c), Ssum);
+        } else {
+#pragma unroll
+          for (int k = 0; k < PPL; ++k) prev[c * PPL + k] = INF16x2;
+        }
+        left_old = P[PPL - 1];
+        if ((nn.um >> c) & 1u) fetch(nn, cn, sn, c);
+      }
+      // per-chain minimum: xor butterfly inside each G-lane group
+      uint32_t hm = min(nmin & 0xFFFFu, nmin >> 16);
+#pragma unroll
+      for (int o = G / 2; o; o >>= 1) hm = min(hm, __shfl_xor_sync(FULL, hm, o));
+      const bool act = cur.spanp != 0u;
+      mp2 = act ? (hm + a.p2i) * 0x10001u : INF16x2;
+      ng = act ? ((0x10000u - hm) & 0xFFFFu) * 0x10001u : INF16x2;
+    };
+    for (int t = 0; t < len; t += 2) {
+      const G4Step s2 = info(t + 2);
+      step(s0, s2, cA, sA);
+      if (t + 1 >= len) break;
+      const G4Step s3 = info(t + 3);
+      step(s1, s3, cB, sB);
+      s0 = s2;
+      s1 = s3;
+    }
+  }
+}
+
+template <int G, int PPL, int MINB>
+static void launch_grp4(const SgmArgs& a, int fam, int init, int n_sv, cudaStream_t st) {
+  const int nchains = fam == FAM_H ? a.H : (fam == FAM_V ? a.W : a.W + a.H - 1);
+  constexpr int per_block = G4_WARPS * (32 / G);
+  dim3 grid((nchains + per_block - 1) / per_block, n_sv);
+  const int nch = (npairs_max(a.d_max) + PPL * G - 1) / (PPL * G);
+  auto go = [&](auto kern) { kern<<<grid, G4_WARPS * 32, 0, st>>>(a, fam, init); };
+  if (nch <= 1) go(k_sgm_grp4<G, 1, PPL, MINB>);
+  else if (nch <= 2) go(k_sgm_grp4<G, 2, PPL, MINB>);
+  else if (nch <= 4) go(k_sgm_grp4<G, 4, PPL, MINB>);
+  else go(k_sgm_grp4<G, 8, PPL, MINB>);
+}
+
 // ------------------------------------------------------------ v4 (u16)
 //
 // Same lane mapping as k_sgm_grp, but the predecessor's path values live in
@@ -1138,6 +1372,37 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
   // st_lo/st_hi[k % parts]; each (seq, view) uses exactly one of lo / hi
   const int np = npairs_max(a.d_max);
   const int fams[4] = {FAM_H, FAM_V, FAM_D1, FAM_D2};
+  static const int g4 = getenv("ES_SGM_G4") ? atoi(getenv("ES_SGM_G4")) : 1;   // A/B switch
+  if (g4) {
+    for (int k = 0; k < 4; ++k) {
+      const int p = k % parts;
+      SgmArgs lo = a, hi = a;
+      lo.select = 1;
+      hi.select = 2;
+      lo.S = S[p];
+      hi.S = S[p];
+      const int init = k < parts;
+      if (np <= 64) {
+        if (g4 == 2) {
+          launch_grp4<4, 2, 4>(lo, fams[k], init, n_sv, st_lo[p]);
+          launch_grp4<8, 2, 1>(hi, fams[k], init, n_sv, st_hi[p]);
+        } else if (g4 == 3) {
+          launch_grp4<8, 4, 1>(lo, fams[k], init, n_sv, st_lo[p]);
+          launch_grp4<8, 4, 1>(hi, fams[k], init, n_sv, st_hi[p]);
+        } else if (g4 == 4) {
+          launch_grp4<4, 4, 3>(lo, fams[k], init, n_sv, st_lo[p]);
+          launch_grp4<8, 4, 1>(hi, fams[k], init, n_sv, st_hi[p]);
+        } else {
+          launch_grp4<4, 4, 4>(lo, fams[k], init, n_sv, st_lo[p]);
+          launch_grp4<8, 4, 1>(hi, fams[k], init, n_sv, st_hi[p]);
+        }
+      } else {
+        launch_grp4<8, 4, 1>(lo, fams[k], init, n_sv, st_lo[p]);
+        launch_grp4<16, 4, 1>(hi, fams[k], init, n_sv, st_hi[p]);
+      }
+    }
+    return;
+  }
   for (int k = 0; k < 4; ++k) {
     const int p = k % parts;
     SgmArgs lo = a, hi = a;
@@ -1168,7 +1433,14 @@ void launch_aggregate(const SgmArgs& a, int arith, int n_sv, cudaStream_t st) {
   int nch = (npairs_max(a.d_max) + 31) / 32;
   if (nch > 4) nch = 8;
   static const bool v1 = getenv("ES_SGM_V1") != nullptr;   // A/B switch for profiling
-  if (arith == ARITH_U16 && !v1) {
+  static const int g4 = getenv("ES_SGM_G4") ? atoi(getenv("ES_SGM_G4")) : 1;   // A/B switch
+  if (arith == ARITH_U16 && !v1 && g4 && !a.lanes) {
+    const int fams[4] = {FAM_H, FAM_V, FAM_D1, FAM_D2};
+    for (int k = 0; k < 4; ++k) {
+      if (npairs_max(a.d_max) <= 64) launch_grp4<4, 4, 4>(a, fams[k], k == 0, n_sv, st);
+      else launch_grp4<8, 4, 1>(a, fams[k], k == 0, n_sv, st);
+    }
+  } else if (arith == ARITH_U16 && !v1) {
     launch_family_seg(a, FAM_H, 3, 1, n_sv, st);
     launch_family_seg(a, FAM_V, 3, 0, n_sv, st);
     launch_family_seg(a, FAM_D1, 3, 0, n_sv, st);

@@ -960,38 +960,25 @@ __global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int
   };
   for (int bwd = 0; bwd < 2; ++bwd) {
     const bool load_sum = !(init && bwd == 0);
-    auto load_meta = [&](int tb) -> uint2 {
+    // chain metadata: every lane loads its chain's pixel itself, four steps
+    // ahead, into the register set of the step's parity (no register
+    // rotation, so nothing waits on a load before its use)
+    auto load_meta = [&](int t) -> uint2 {
       int x, y;
-      const int t = tb + gl;
       if (t < len && grp_pixel(fam, bwd, ch, t, W, H, x, y)) return meta[(size_t)y * W + x];
       return make_uint2(NONE, 0u);
     };
-    uint2 mb_cur = load_meta(0);
-    uint2 mb_next = load_meta(G);
-    uint2 mb_next2 = load_meta(2 * G);
-    int tb = 0;
-    auto info = [&](int tp) -> G4Step {
+    auto info = [&](uint2 mt) -> G4Step {
       G4Step s{0, 0, 0u, 0u};
       int clo = NCH, chi = -1;
-      if (tp < len) {
-        if (tp == tb + G) {
-          tb += G;
-          mb_cur = mb_next;
-          mb_next = mb_next2;
-          mb_next2 = load_meta(tb + 2 * G);
-        }
-        const int r = tp - tb;
-        const uint32_t mx = __shfl_sync(FULL, mb_cur.x, gbase | r);
-        const uint32_t my = __shfl_sync(FULL, mb_cur.y, gbase | r);
-        if (mx != NONE) {
-          const int j0 = (int)((mx & 0xFFFFu) >> 1);
-          const int j1 = (int)((mx >> 16) >> 1);
-          s.base = (int)(my - (uint32_t)j0) + PPL * gl;
-          s.relb = PPL * gl - j0 + PPL - 1;
-          s.spanp = (uint32_t)(j1 - j0 + PPL);
-          clo = j0 / CW;
-          chi = j1 / CW;
-        }
+      if (mt.x != NONE) {
+        const int j0 = (int)((mt.x & 0xFFFFu) >> 1);
+        const int j1 = (int)((mt.x >> 16) >> 1);
+        s.base = (int)(mt.y - (uint32_t)j0) + PPL * gl;
+        s.relb = PPL * gl - j0 + PPL - 1;
+        s.spanp = (uint32_t)(j1 - j0 + PPL);
+        clo = j0 / CW;
+        chi = j1 / CW;
       }
       s.um = umask(__reduce_min_sync(FULL, clo), __reduce_max_sync(FULL, chi));
       return s;
@@ -1005,8 +992,11 @@ __global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int
       Vec<PPL>::ld(S + s.base + c * CW, p && load_sum, &sn[c * PPL]);
     };
     uint32_t prev[NW], cA[NW], sA[NW], cB[NW], sB[NW];
-    G4Step s0 = info(0);
-    G4Step s1 = info(1);
+    uint2 mA = load_meta(0), mB = load_meta(1);
+    G4Step s0 = info(mA);
+    G4Step s1 = info(mB);
+    mA = load_meta(2);
+    mB = load_meta(3);
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
 #pragma unroll
@@ -1069,10 +1059,12 @@ __global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int
       ng = act ? ((0x10000u - hm) & 0xFFFFu) * 0x10001u : INF16x2;
     };
     for (int t = 0; t < len; t += 2) {
-      const G4Step s2 = info(t + 2);
+      const G4Step s2 = info(mA);
+      mA = load_meta(t + 4);
       step(s0, s2, cA, sA);
       if (t + 1 >= len) break;
-      const G4Step s3 = info(t + 3);
+      const G4Step s3 = info(mB);
+      mB = load_meta(t + 5);
       step(s1, s3, cB, sB);
       s0 = s2;
       s1 = s3;

@@ -21,6 +21,7 @@
 namespace es {
 
 constexpr int COST_NT = 256;
+constexpr unsigned FULL = 0xffffffffu;
 
 template <int NW>
 __global__ void __launch_bounds__(COST_NT) k_cost(CostArgs a) {
@@ -230,7 +231,156 @@ __global__ void __launch_bounds__(COST_NT) k_cost_w3(CostArgs a) {
   }
 }
 
+// Window 3, run-table schedule.  Every pixel's allocation is a whole number
+// of aligned 4-pair runs (8 cells, one 16-byte word; es_common.cuh), and a
+// row's allocations are consecutive, so a warp that owns 32 consecutive
+// pixels owns a contiguous range of runs.  The warp scans its pixels' run
+// counts, writes the owning lane of every run into a per-warp table in
+// shared memory, and then lane l computes runs l, l+32, ...: stores are
+// fully coalesced 16-byte words and no thread searches for its pixel.  A run
+// needs the three reference columns of its pixel and ten columns of the
+// other image (3 VABSDIFF4 per cell on three rows packed in bytes); runs
+// that touch the image border or the interval ends take the per-cell path.
+constexpr int CR_WARPS = 8;
+
+// columns of edge replication on each side of the other image's row buffer:
+// covers every match column x + ox +- d of a run (|d| <= d_max, run of 8)
+__host__ __device__ inline int cost_pad_cols(int d_max) { return ((d_max + 8) & ~7) + 8; }
+
+template <int SIGN>
+__device__ __forceinline__ void cost_runs_row(const CostArgs& a, int rmax);
+
+__global__ void __launch_bounds__(CR_WARPS * 32) k_cost_runs(CostArgs a, int rmax) {
+  // the match direction is a compile-time constant of each specialised body
+  if (((a.view0 + (int)blockIdx.y) & 1) == 0) cost_runs_row<-1>(a, rmax);
+  else cost_runs_row<1>(a, rmax);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void cost_runs_row(const CostArgs& a, int rmax) {
+  extern __shared__ uint32_t sm[];
+  const int W = a.W, H = a.H;
+  const int y = blockIdx.x;
+  const int svl = blockIdx.y;
+  const int svg = a.view0 + svl;
+  const int view = svg & 1, seq = svg >> 1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int PADC = cost_pad_cols(a.d_max);
+  uint32_t* refcol = sm;                                   // [W]
+  uint32_t* othpad = sm + W;                               // [W + 2 PADC], column k at k + PADC
+  uint8_t* tab = reinterpret_cast<uint8_t*>(sm + 2 * W + 2 * PADC) + wid * 32 * rmax;
+  const size_t HW = (size_t)W * H;
+  const uint8_t* ref = a.img + ((size_t)seq * 2 + view) * HW;
+  const uint8_t* oth = a.img + ((size_t)seq * 2 + (view ^ 1)) * HW;
+  const uint2* meta = a.meta + (size_t)svl * HW + (size_t)y * W;
+  const uint32_t rowbase = (uint32_t)(y * row_capacity(W, a.d_max));
+  const int y0 = max(y - 1, 0), y2 = min(y + 1, H - 1);
+  for (int x = threadIdx.x; x < W; x += CR_WARPS * 32)
+    refcol[x] = (uint32_t)ref[(size_t)y0 * W + x] | ((uint32_t)ref[(size_t)y * W + x] << 8) |
+                ((uint32_t)ref[(size_t)y2 * W + x] << 16);
+  for (int k = threadIdx.x; k < W + 2 * PADC; k += CR_WARPS * 32) {
+    const int x = clampi(k - PADC, 0, W - 1);
+    othpad[k] = (uint32_t)oth[(size_t)y0 * W + x] | ((uint32_t)oth[(size_t)y * W + x] << 8) |
+                ((uint32_t)oth[(size_t)y2 * W + x] << 16);
+  }
+  __syncthreads();
+  const uint32_t border = 9u * 255u;
+  uint4* C4 = reinterpret_cast<uint4*>(a.C + (size_t)svl * a.volcap + rowbase);
+  constexpr int sign = SIGN;
+  for (int gx = wid * 32; gx < W; gx += CR_WARPS * 32) {
+    const int x = gx + lane;
+    int lo = 0, hi = -1, nrun = 0;
+    uint32_t run0 = 0;   // row-relative run index of the pixel's allocation
+    if (x < W) {
+      const uint2 mt = meta[x];
+      lo = (int)lo_of(mt);
+      hi = (int)hi_of(mt);
+      run0 = (mt.y - rowbase - pad_before(lo)) >> 2;
+      nrun = (int)(pixel_slots(lo, hi) >> 2);
+    }
+    int incl = nrun;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int excl = incl - nrun;
+    const int total = __shfl_sync(FULL, incl, 31);
+    const uint32_t grun0 = __shfl_sync(FULL, run0, 0);
+    for (int j = 0; j < nrun; ++j) tab[excl + j] = (uint8_t)lane;
+    __syncwarp();
+    for (int r0 = 0; r0 < total; r0 += 32) {
+      const int r = r0 + lane;
+      const bool live = r < total;
+      const int p = live ? tab[r] : 0;
+      const int plo = __shfl_sync(FULL, lo, p);
+      const int phi = __shfl_sync(FULL, hi, p);
+      const int pex = __shfl_sync(FULL, excl, p);
+      const int px = gx + p;
+      const int dbase = (plo & ~7) + (live ? 8 * (r - pex) : 0);   // idle lanes: a valid run
+      uint32_t c[8];
+      if (px >= 1 && px <= W - 2) {
+        // interior pixel: the window's columns x-1..x+1 are unclamped, so the
+        // clamped match column of (ox, d) is the edge-replicated buffer entry
+        // x + ox + sign*d, shared by neighbouring cells
+        const uint32_t r0c = refcol[px - 1], r1c = refcol[px], r2c = refcol[px + 1];
+        const int cbase = sign < 0 ? px - 1 - (dbase + 7) : px - 1 + dbase;
+        const uint32_t* ob = othpad + PADC + cbase;
+        uint32_t o[10];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) o[k] = ob[k];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          // left view: cell dbase+i uses columns cbase + 7-i .. 9-i; right
+          // view: cbase + i .. i+2
+          const int k = sign < 0 ? 7 - i : i;
+          c[i] = __vsadu4(r2c, o[k + 2]) + (__vsadu4(r1c, o[k + 1]) + __vsadu4(r0c, o[k]));
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int d = dbase + i;
+          uint32_t sad = 0;
+#pragma unroll
+          for (int ox = -1; ox <= 1; ++ox) {
+            const int xx = clampi(px + ox, 0, W - 1);
+            sad = __vsadu4(refcol[xx], othpad[PADC + clampi(xx + sign * d, 0, W - 1)]) + sad;
+          }
+          c[i] = sad;
+        }
+      }
+      // interval ends (+inf) and off-image match centres (border cost)
+      const int xm_far = px + sign * (dbase + 7), xm_near = px + sign * dbase;
+      const bool fix = dbase < plo || dbase + 7 > phi || xm_far < 0 || xm_far > W - 1 ||
+                       xm_near < 0 || xm_near > W - 1;
+      if (__any_sync(FULL, fix)) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int d = dbase + i;
+          const int xm = px + sign * d;
+          if ((unsigned)xm > (unsigned)(W - 1)) c[i] = border;
+          if (d < plo || d > phi) c[i] = INF16;
+        }
+      }
+      if (live)
+        C4[grun0 + r] = make_uint4(c[0] | (c[1] << 16), c[2] | (c[3] << 16), c[4] | (c[5] << 16),
+                                   c[6] | (c[7] << 16));
+    }
+    __syncwarp();
+  }
+}
+
 void launch_cost(const CostArgs& a, int n_sv, cudaStream_t st) {
+  static const bool runs = getenv("ES_COST_W3") == nullptr;   // A/B switch
+  if (a.window == 3 && runs) {
+    const int rmax = (npairs_max(a.d_max) + 3) / 4;   // runs per pixel, at most
+    dim3 grid(a.H, n_sv);
+    const size_t smem = sizeof(uint32_t) * (2 * (size_t)a.W + 2 * (size_t)cost_pad_cols(a.d_max)) +
+                        (size_t)CR_WARPS * 32 * rmax;
+    cudaFuncSetAttribute(k_cost_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_cost_runs<<<grid, CR_WARPS * 32, smem, st>>>(a, rmax);
+    return;
+  }
   if (a.window == 3 && getenv("ES_COST_V1") == nullptr) {
     dim3 grid(a.H, n_sv);
     const size_t smem = sizeof(uint32_t) * (4 * (size_t)a.W + 1);

@@ -970,6 +970,7 @@ int es_select_disparity(const float* vol, int H, int W, int D, double* d, uint8_
   wa.meta = meta;
   wa.S = rag;
   wa.volcap = (size_t)H * row_capacity(W, D - 1);
+  wa.d_max = D - 1;
   wa.arith = f32 ? ARITH_F32 : ARITH_U16;
   wa.s_max = 1.0;
   wa.r_min = 1.0;

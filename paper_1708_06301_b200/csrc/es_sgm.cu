@@ -1660,7 +1660,127 @@ __global__ void __launch_bounds__(256) k_wta_var_u16g(WtaArgs a) {
   }
 }
 
+// u16 sums, run-table schedule (as k_cost_runs): a warp owns 32 consecutive
+// pixels of a view, lane l streams runs l, l+32, ... of their allocations
+// (one coalesced 16-byte word per partial sum, 8 cells), forms
+// (value << 16 | d) keys for the cells inside [lo, hi], reduces them over the
+// pixel's lanes with a segmented shuffle minimum and a shared-memory
+// atomicMin (pixels whose runs span iterations), and finally every lane
+// walks outward from its own pixel's winner (sgm.py:282, 319-344) over
+// L1-resident data.
+constexpr int WR_WARPS = 8;
+
+template <int N>
+__global__ void __launch_bounds__(WR_WARPS * 32) k_wta_runs(WtaArgs a, int rmax) {
+  extern __shared__ uint32_t wsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t* key = wsm + wid * 32;
+  uint8_t* tab = reinterpret_cast<uint8_t*>(wsm + WR_WARPS * 32) + wid * 32 * rmax;
+  const size_t HW = (size_t)a.W * a.H;
+  const int svl = blockIdx.y;
+  const uint2* meta = a.meta + (size_t)svl * HW;
+  const uint4* Sv[N];
+  Sv[0] = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(a.S) + (size_t)svl * a.volcap);
+#pragma unroll
+  for (int i = 1; i < N; ++i)
+    Sv[i] = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(a.Sx[i - 1]) + (size_t)svl * a.volcap);
+  const size_t ngroups = (HW + 31) / 32;
+  for (size_t g = (size_t)blockIdx.x * WR_WARPS + wid; g < ngroups; g += (size_t)gridDim.x * WR_WARPS) {
+    const size_t pix = g * 32 + lane;
+    uint2 mt = make_uint2(0u, 0u);
+    int lo = 0, hi = -1, nrun = 0;
+    uint32_t run0 = 0;
+    if (pix < HW) {
+      mt = meta[pix];
+      lo = (int)lo_of(mt);
+      hi = (int)hi_of(mt);
+      run0 = (mt.y - pad_before(lo)) >> 2;
+      nrun = (int)(pixel_slots(lo, hi) >> 2);
+    }
+    int incl = nrun;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int excl = incl - nrun;
+    const int total = __shfl_sync(FULL, incl, 31);
+    for (int j = 0; j < nrun; ++j) tab[excl + j] = (uint8_t)lane;
+    key[lane] = 0xFFFFFFFFu;
+    __syncwarp();
+    for (int r0 = 0; r0 < total; r0 += 32) {
+      const int r = r0 + lane;
+      const bool live = r < total;
+      const int p = live ? tab[r] : 31;
+      const int plo = __shfl_sync(FULL, lo, p);
+      const int phi = __shfl_sync(FULL, hi, p);
+      const int pex = __shfl_sync(FULL, excl, p);
+      const uint32_t prun = __shfl_sync(FULL, run0, p);
+      uint32_t best = 0xFFFFFFFFu;
+      if (live) {
+        const int j = r - pex;
+        uint4 w = Sv[0][prun + j];
+#pragma unroll
+        for (int i = 1; i < N; ++i) {
+          const uint4 v = Sv[i][prun + j];
+          w = make_uint4(__vadd2(w.x, v.x), __vadd2(w.y, v.y), __vadd2(w.z, v.z), __vadd2(w.w, v.w));
+        }
+        const uint32_t d0 = (uint32_t)((plo & ~7) + 8 * j);
+        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+        uint32_t k[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          k[2 * q] = (ww[q] << 16) | (d0 + 2 * q);
+          k[2 * q + 1] = (ww[q] & 0xFFFF0000u) | (d0 + 2 * q + 1);
+        }
+        if ((int)d0 < plo || (int)d0 + 7 > phi) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if ((int)d0 + i < plo || (int)d0 + i > phi) k[i] = 0xFFFFFFFFu;
+        }
+        best = min(min(min(k[0], k[1]), min(k[2], k[3])), min(min(k[4], k[5]), min(k[6], k[7])));
+      }
+      // segmented minimum over the lanes of one pixel (contiguous lanes)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t ob = __shfl_down_sync(FULL, best, o);
+        const int op = __shfl_down_sync(FULL, p, o);
+        if (lane + o < 32 && op == p) best = min(best, ob);
+      }
+      const int pp = __shfl_up_sync(FULL, p, 1);
+      if (live && (lane == 0 || pp != p)) atomicMin(&key[p], best);
+    }
+    __syncwarp();
+    if (pix < HW) {
+      const SumRows<N> s = sum_rows<N>(a, (size_t)svl * a.volcap + mt.y);
+      wta_finish(a, s, lo, hi, lo >> 1, key[lane], (size_t)svl * HW + pix);
+    }
+    __syncwarp();
+  }
+}
+
 void launch_wta_variance(const WtaArgs& a, int n_sv, cudaStream_t st) {
+  static const bool runs = getenv("ES_WTA_OLD") == nullptr;   // A/B switch
+  if (runs && a.arith == ARITH_U16 && a.dstar_in == nullptr) {
+    const size_t HW = (size_t)a.W * a.H;
+    const int nparts = 1 + (a.Sx[0] != nullptr) + (a.Sx[1] != nullptr) + (a.Sx[2] != nullptr);
+    const int rmax = (npairs_max(a.d_max) + 3) / 4;
+    const size_t smem = sizeof(uint32_t) * WR_WARPS * 32 + (size_t)WR_WARPS * 32 * rmax;
+    const size_t groups = (HW + 31) / 32;
+    // blocks per (seq, view): enough that the whole batch fills every SM a few times
+    const unsigned per_sv = (unsigned)std::min<size_t>((groups + WR_WARPS - 1) / WR_WARPS,
+                                                       std::max<size_t>(16, (148 * 8 + n_sv - 1) / n_sv));
+    dim3 grid(per_sv, n_sv);
+    auto go = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kern<<<grid, WR_WARPS * 32, smem, st>>>(a, rmax);
+    };
+    if (nparts == 1) go(k_wta_runs<1>);
+    else if (nparts == 2) go(k_wta_runs<2>);
+    else if (nparts == 3) go(k_wta_runs<3>);
+    else go(k_wta_runs<4>);
+    return;
+  }
   const size_t HW = (size_t)a.W * a.H;
   if (a.arith == ARITH_U16 && a.dstar_in == nullptr) {
     const int nparts = 1 + (a.Sx[0] != nullptr) + (a.Sx[1] != nullptr) + (a.Sx[2] != nullptr);

@@ -84,6 +84,19 @@ def measured_traffic(config, batch, texture_scale):
     return None
 
 
+def stage_roofline(nbytes, ms, peak):
+    gbs = nbytes / (ms / 1e3) / 1e9 if ms > 0 else None
+    return {"bytes_per_step": nbytes, "ms_per_step": ms, "achieved": gbs, "unit": "GB/s",
+            "frac": gbs / peak if gbs else None}
+
+
+def traffic_line(traffic, ms, peak):
+    if not traffic or ms <= 0:
+        return None
+    gbs = traffic / (ms / 1e3) / 1e9
+    return {"dram_bytes_per_step": traffic, "achieved": gbs, "unit": "GB/s", "frac": gbs / peak}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -360,6 +373,16 @@ def main():
                      "traffic": measured_traffic(args.config, B, TEXTURE_SCALE),
                      "traffic_unit": "bytes per step (all sequences, both views)",
                      "peak_kind": peak_kind, "bytes_per_step": agg_bytes},
+        # the multi-pass aggregation reads C and read-modify-writes a partial
+        # sum once per direction: its DRAM traffic / stage time is the
+        # bandwidth it actually sustains
+        "aggregation_dram": traffic_line(measured_traffic(args.config, B, TEXTURE_SCALE), agg_ms, peak),
+        # the other SURVEY 8(d) kernels on their algorithmic bytes
+        "roofline_stages": {
+            "cost": stage_roofline(2 * hw * 2 * B + 8 * hw * 2 * B + 2 * cells,
+                                   stage[2] / max(nsteps.value, 1), peak),
+            "wta_variance": stage_roofline(2 * cells + 11 * hw * 2 * B,
+                                           stage[4] / max(nsteps.value, 1), peak)},
         "pipeline_roofline": {"achieved": frame_bytes / (ms_max / K / 1e3) / 1e9,
                               "frac": frame_bytes / (ms_max / K / 1e3) / 1e9 / peak},
         "gpu_launches": KERNELS_PER_STEP * K,

@@ -114,25 +114,31 @@ def sequence_specs(n, seed0):
                                  yaw_deg=CFG["yaw_deg"]) for s in range(n)]
 
 
-def render_frames(specs, frames, device):
-    """Device images [len(frames)][B][2][H][W] (torch uint8)."""
+def render_frames(specs, frames, device, rig=None, with_gt=False):
+    """Device images [len(frames)][B][2][H][W] (torch uint8); with ``with_gt``
+    also the rendered ground-truth disparities (float64, same shape)."""
     import torch
     from paper_1708_06301_b200 import _lib
     from paper_1708_06301_b200.core import StereoRig
-    rig = _lib.rig_struct(StereoRig(**RIG))
+    rig = rig or StereoRig(**RIG)
+    h, w = rig.height, rig.width
+    rs = _lib.rig_struct(rig)
     B = len(specs)
     n_box = specs[0][0].shape[0]
     boxes = np.ascontiguousarray(np.stack([sp[0] for sp in specs]), np.float64)
     seeds = np.arange(B, dtype=np.int64) + 17
-    out = torch.empty((len(frames), B, 2, H, W), dtype=torch.uint8, device=device)
+    out = torch.empty((len(frames), B, 2, h, w), dtype=torch.uint8, device=device)
+    gt = (torch.empty((len(frames), B, 2, h, w), dtype=torch.float64, device=device)
+          if with_gt else None)
     stream = torch.cuda.current_stream(device).cuda_stream
     for i, k in enumerate(frames):
         poses = np.ascontiguousarray(np.stack([sp[1][k % SEQ_FRAMES] for sp in specs]), np.float64)
-        _lib.call("es_render", ctypes.byref(rig), _lib.ptr(boxes), n_box, _lib.ptr(poses),
+        _lib.call("es_render", ctypes.byref(rs), _lib.ptr(boxes), n_box, _lib.ptr(poses),
                   _lib.ptr(seeds), B, ctypes.c_double(TEXTURE_SCALE), 12,
-                  ctypes.c_void_p(out[i].data_ptr()), None, ctypes.c_void_p(stream))
+                  ctypes.c_void_p(out[i].data_ptr()),
+                  ctypes.c_void_p(gt[i].data_ptr()) if with_gt else None, ctypes.c_void_p(stream))
     torch.cuda.synchronize(device)
-    return out
+    return (out, gt) if with_gt else out
 
 
 def motions_for(specs, k):

@@ -149,6 +149,23 @@ int es_reject_edges(const double* d, const uint8_t* valid, int H, int W, double 
  * (x, y, d) triples; out (n, 3) */
 int es_warp_points(const double* Hm, const double* pts, int n, double* out);
 
+/* ---- evaluation metrics (metrics.py:39-117) -------------------------------
+ * metrics.bad_pixel_rate / bad_pixel_mask / error_image / density on n_maps
+ * host maps of n pixels ([n_maps][n], f64 values + u8 valid); mode 0 = "or"
+ * (|err| > 3 px OR > 5 %), 1 = "and" (KITTI 2015).
+ *   counts [n_maps][4]: ground-truth valid, jointly valid, bad, estimate valid
+ *   mask   optional [n_maps][n] u8 (bad_pixel_mask), rgb optional
+ *          [n_maps][n][3] u8 (error_image); NULL to skip                    */
+int es_bad_pixel_counts(const double* est, const uint8_t* est_valid, const double* gt,
+                        const uint8_t* gt_valid, int64_t n, int n_maps, int mode,
+                        uint64_t* counts, uint8_t* mask, uint8_t* rgb);
+/* the same counts for every sequence's fused map of `view` in a context,
+ * against device ground truth (sequence s at gt_dev + s * gt_stride, H*W
+ * values); counts is host [batch][4]; enqueued on the context's stream
+ * behind any deferred step and synchronised once (one 32*batch-byte read) */
+int es_ctx_metrics(es_ctx* ctx, int view, const double* gt_dev, const uint8_t* gt_valid_dev,
+                   int64_t gt_stride, int mode, uint64_t* counts);
+
 /* ---- synthetic input renderer (synth.py:87-218 restated, boxes only) ---- */
 /* boxes [n_seq][n_box][6], poses [n_seq][16], seeds [n_seq]; out_dev images
  * [n_seq][2][H][W] (device); gt_dev optional [n_seq][2][H][W] f64 (device) */

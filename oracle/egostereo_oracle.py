@@ -18,6 +18,9 @@ import numpy as np
 
 __all__ = [
     "OracleParams",
+    "bad_mask",
+    "bad_rate",
+    "error_rgb",
     "border_cost",
     "full_intervals",
     "predicted_intervals",
@@ -413,6 +416,47 @@ def fill_holes(d, p, v, gamma_f: float, q: float):
     d, p, v = _fill_pass(d, p, v, gamma_f, q, axis=1)
     d, p, v = _fill_pass(d, p, v, gamma_f, q, axis=0)
     return np.where(v, d, 0.0), p, v
+
+
+# --------------------------------------------------------------------------
+# evaluation metrics (metrics.py:39-103)
+# --------------------------------------------------------------------------
+
+ABS_THRESHOLD = 3.0      # metrics.py:20
+REL_THRESHOLD = 0.05     # metrics.py:21
+
+
+def bad_mask(est_d, est_v, gt_d, gt_v, mode: str = "or"):
+    """metrics.py:81-92: bad over the jointly valid region; "or" flags
+    |err| > 3 px OR > 5 % of the true disparity, "and" requires both."""
+    err = np.abs(est_d - gt_d)
+    over_abs = err > ABS_THRESHOLD
+    over_rel = err > REL_THRESHOLD * gt_d
+    bad = (over_abs | over_rel) if mode == "or" else (over_abs & over_rel)
+    return bad & est_v & gt_v
+
+
+def bad_rate(est_d, est_v, gt_d, gt_v, mode: str = "or"):
+    """metrics.py:39-78: (rate over jointly valid, rate counting missed
+    ground-truth pixels as bad, ground-truth coverage)."""
+    n_gt = int(gt_v.sum())
+    if n_gt == 0:
+        return 0.0, 0.0, 0.0
+    both = gt_v & est_v
+    n_both = int(both.sum())
+    n_bad = int(bad_mask(est_d, est_v, gt_d, gt_v, mode).sum())
+    rate = n_bad / n_both if n_both else 0.0
+    return rate, (n_bad + n_gt - n_both) / n_gt, n_both / n_gt
+
+
+def error_rgb(est_d, est_v, gt_d, gt_v, mode: str = "or"):
+    """metrics.py:106-117: blue within threshold, red bad, black no data."""
+    img = np.zeros(est_d.shape + (3,), dtype=np.uint8)
+    both = est_v & gt_v
+    bad = bad_mask(est_d, est_v, gt_d, gt_v, mode)
+    img[both & ~bad] = (40, 90, 220)
+    img[bad] = (220, 50, 40)
+    return img
 
 
 # --------------------------------------------------------------------------

@@ -318,8 +318,74 @@ def gen_config1():
     save("config1", **out)
 
 
+def gen_metrics():
+    """Evaluation metrics (metrics.py) on seeded maps, and the reference's
+    run_sequence output tree (metrics.txt, summary.txt, disp_0 / err_0
+    arrays) for a small rendered sequence with ground truth."""
+    from egostereo import metrics
+    import tempfile
+
+    import cv2
+    out = {}
+    rng = np.random.default_rng(11)
+    for case, (h, w) in enumerate([(7, 9), (31, 45), (64, 3), (5, 5)]):
+        gt = rng.uniform(0.5, 60.0, (h, w))
+        gv = rng.random((h, w)) < 0.7
+        est = gt + rng.normal(0.0, 2.5, (h, w)) * (rng.random((h, w)) < 0.6)
+        # exact threshold ties: |err| == 3 and |err| == 0.05 * gt
+        est.flat[::7] = gt.flat[::7] + 3.0
+        est.flat[1::11] = gt.flat[1::11] * 1.05
+        ev = rng.random((h, w)) < 0.8
+        if case == 3:
+            gv[:] = False
+        gt = np.where(gv, gt, 0.0)
+        est = np.where(ev, est, 0.0)
+        e, t = core.DisparityMap(est, ev), core.DisparityMap(gt, gv)
+        out[f"c{case}_est"], out[f"c{case}_ev"] = est, ev
+        out[f"c{case}_gt"], out[f"c{case}_gv"] = gt, gv
+        out[f"c{case}_density"] = np.array(metrics.density(e))
+        for mode in ("or", "and"):
+            r = metrics.bad_pixel_rate(e, t, mode)
+            out[f"c{case}_{mode}_rates"] = np.array([r.rate, r.rate_all, r.density])
+            out[f"c{case}_{mode}_mask"] = metrics.bad_pixel_mask(e, t, mode)
+            out[f"c{case}_{mode}_rgb"] = metrics.error_image(e, t, mode)
+    save("metrics", **out)
+
+    # run_sequence over a small rendered sequence with ground truth
+    rig = rig_small(64, 40, 16, f=48.0, b=0.5)
+    scene = synth.SceneSpec(
+        rig=rig,
+        primitives=(synth.Plane(z=4.0),
+                    synth.Box(x0=-0.6, x1=0.3, y0=-0.4, y1=0.5, z0=2.0, z1=2.5)),
+        texture_seed=4,
+    )
+    traj = synth.dolly_trajectory(3, -0.06)
+    frames = synth.make_sequence(scene, traj, sigma_rot_deg=0.05, sigma_trans=0.005, seed=6)
+    seq = pipeline.Sequence(rig, [f.left for f in frames], [f.right for f in frames],
+                            [f.motion_noisy for f in frames],
+                            gt_left=[f.gt_left for f in frames],
+                            gt_right=[f.gt_right for f in frames])
+    out = {"rig": np.array([rig.f, rig.b, rig.cx, rig.cy, rig.width, rig.height, rig.d_max])}
+    for k, f in enumerate(frames):
+        out[f"f{k}_left"], out[f"f{k}_right"] = f.left.data, f.right.data
+        out[f"f{k}_motion"] = np.eye(4) if f.motion_noisy is None else f.motion_noisy
+        out[f"f{k}_has_motion"] = np.array(f.motion_noisy is not None)
+        out[f"f{k}_gt_d"], out[f"f{k}_gt_v"] = f.gt_left.values, f.gt_left.valid
+        out[f"f{k}_gtr_d"], out[f"f{k}_gtr_v"] = f.gt_right.values, f.gt_right.valid
+    with tempfile.TemporaryDirectory() as tmp:
+        pipeline.run_sequence(seq, out_dir=tmp, metric_mode="or")
+        out["metrics_txt"] = np.array(open(os.path.join(tmp, "metrics.txt")).read())
+        out["summary_txt"] = np.array(open(os.path.join(tmp, "summary.txt")).read())
+        for k in range(len(frames)):
+            out[f"f{k}_disp_png"] = cv2.imread(os.path.join(tmp, "disp_0", f"{k:06d}.png"),
+                                               cv2.IMREAD_UNCHANGED)
+            out[f"f{k}_err_png"] = cv2.imread(os.path.join(tmp, "err_0", f"{k:06d}.png"),
+                                              cv2.IMREAD_UNCHANGED)
+    save("run_sequence", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["cost_agg", "misc", "prediction", "sequences", "config1"]
+    which = sys.argv[1:] or ["cost_agg", "misc", "prediction", "sequences", "config1", "metrics"]
     if "cost_agg" in which:
         gen_cost_agg()
     if "misc" in which:
@@ -330,3 +396,5 @@ if __name__ == "__main__":
         gen_sequences()
     if "config1" in which:
         gen_config1()
+    if "metrics" in which:
+        gen_metrics()

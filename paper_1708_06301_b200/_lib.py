@@ -47,6 +47,7 @@ class EsParams(ctypes.Structure):
 _P = ctypes.c_void_p
 _I = ctypes.c_int
 _D = ctypes.c_double
+_L = ctypes.c_int64
 
 # symbol -> argtypes (every entry point declared in include/egostereo_b200.h)
 SIGNATURES = {
@@ -81,6 +82,8 @@ SIGNATURES = {
     "es_reject_edges": [_P, _P, _I, _I, _D, _I, _P],
     "es_warp_points": [_P, _P, _I, _P],
     "es_render": [_P, _P, _I, _P, _P, _I, _D, _I, _P, _P, _P],
+    "es_bad_pixel_counts": [_P, _P, _P, _P, _L, _I, _I, _P, _P, _P],
+    "es_ctx_metrics": [_P, _I, _P, _P, _L, _I, _P],
 }
 
 _lib = None

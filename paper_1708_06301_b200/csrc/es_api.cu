@@ -1205,3 +1205,60 @@ int es_render(const es_rig* rig, const double* boxes, int n_box, const double* p
 }
 
 }  // extern "C"
+
+// ---- evaluation metrics (metrics.py:39-117) ----------------------------------
+extern "C" int es_bad_pixel_counts(const double* est, const uint8_t* est_valid, const double* gt,
+                                   const uint8_t* gt_valid, int64_t n, int n_maps, int mode,
+                                   uint64_t* counts, uint8_t* mask, uint8_t* rgb) {
+  if (n < 0 || n_maps < 0) return fail(ES_ERR_VALUE, "bad map size");
+  if (mode != 0 && mode != 1) return fail(ES_ERR_VALUE, "mode must be 'or' or 'and'");
+  if (n_maps == 0) return ES_OK;
+  const size_t N = (size_t)n * n_maps;
+  Scratch s;
+  MetricsArgs a;
+  a.est = s.up(est, N);
+  a.est_valid = s.up(est_valid, N);
+  a.gt = s.up(gt, N);
+  a.gt_valid = s.up(gt_valid, N);
+  a.counts = s.get<unsigned long long>(4 * (size_t)n_maps);
+  a.mask = mask ? s.get<uint8_t>(N) : nullptr;
+  a.rgb = rgb ? s.get<uint8_t>(3 * N) : nullptr;
+  NEED(a.est && a.est_valid && a.gt && a.gt_valid && a.counts && (!mask || a.mask) &&
+       (!rgb || a.rgb));
+  a.n = (size_t)n;
+  a.stride_e = a.stride_g = (size_t)n;
+  a.mode = mode;
+  CK(cudaMemset(a.counts, 0, sizeof(unsigned long long) * 4 * n_maps));
+  if (n) launch_metrics(a, n_maps, 0);
+  DONE();
+  CK(cudaMemcpy(counts, a.counts, sizeof(uint64_t) * 4 * n_maps, cudaMemcpyDeviceToHost));
+  if (mask) CK(cudaMemcpy(mask, a.mask, N, cudaMemcpyDeviceToHost));
+  if (rgb) CK(cudaMemcpy(rgb, a.rgb, 3 * N, cudaMemcpyDeviceToHost));
+  return ES_OK;
+}
+
+extern "C" int es_ctx_metrics(es_ctx* c, int view, const double* gt_dev, const uint8_t* gt_valid_dev,
+                              int64_t gt_stride, int mode, uint64_t* counts) {
+  if (view < 0 || view > 1) return fail(ES_ERR_VALUE, "view must be 0 or 1");
+  if (mode != 0 && mode != 1) return fail(ES_ERR_VALUE, "mode must be 'or' or 'and'");
+  CK(cudaSetDevice(c->device));
+  unsigned long long* dc = nullptr;
+  CK(cudaMallocAsync((void**)&dc, sizeof(unsigned long long) * 4 * c->B, c->st));
+  CK(cudaMemsetAsync(dc, 0, sizeof(unsigned long long) * 4 * c->B, c->st));
+  MetricsArgs a;
+  a.est = c->sd[c->cur] + (size_t)view * c->HW;
+  a.est_valid = c->sv[c->cur] + (size_t)view * c->HW;
+  a.gt = gt_dev;
+  a.gt_valid = gt_valid_dev;
+  a.n = c->HW;
+  a.stride_e = 2 * c->HW;
+  a.stride_g = (size_t)gt_stride;
+  a.mode = mode;
+  a.counts = dc;
+  launch_metrics(a, c->B, c->st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(counts, dc, sizeof(uint64_t) * 4 * c->B, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaFreeAsync(dc, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return ES_OK;
+}

@@ -146,6 +146,20 @@ void launch_fill_axis(const double* d, const double* p, const uint8_t* v, int W,
 void launch_intervals_only(const double* d, const double* p, const uint8_t* v, int n, int d_max,
                            int64_t* lo, int64_t* hi, cudaStream_t st);
 
+// ---- evaluation metrics (es_metrics.cu) --------------------------------------
+struct MetricsArgs {
+  const double* est;          // [n_maps][stride_e]
+  const uint8_t* est_valid;
+  const double* gt;           // [n_maps][stride_g]
+  const uint8_t* gt_valid;
+  size_t n, stride_e, stride_g;
+  int mode;                   // 0 "or", 1 "and"
+  unsigned long long* counts; // [n_maps][4]: gt valid, jointly valid, bad, estimate valid
+  uint8_t* mask = nullptr;    // optional [n_maps][n]
+  uint8_t* rgb = nullptr;     // optional [n_maps][n][3]
+};
+void launch_metrics(const MetricsArgs& a, int n_maps, cudaStream_t st);
+
 // ---- synthetic renderer (es_render.cu) -------------------------------------
 struct RenderArgs {
   Rig rig;

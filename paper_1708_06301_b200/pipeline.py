@@ -315,6 +315,21 @@ class BatchedPipeline:
     def result(self, seq: int) -> FrameResult:
         return FrameResult(self.engine, seq, self.engine.frame(seq))
 
+    def metrics(self, gt_dev: int, gt_valid_dev: int, gt_stride: int, view: int = 0,
+                mode: str = "or"):
+        """Per-sequence evaluation of the current fused maps against device
+        ground truth (sequence s at ``gt_dev + s * gt_stride`` float64 values
+        and ``gt_valid_dev + s * gt_stride`` uint8 flags): a list of
+        (metrics.BadPixelResult, density) -- metrics.py:39-97 on the device,
+        one 32-byte-per-sequence read back."""
+        from . import metrics as M
+        counts = np.zeros((self.batch, 4), np.uint64)
+        _lib.call("es_ctx_metrics", self.engine._h, int(view), ctypes.c_void_p(gt_dev),
+                  ctypes.c_void_p(gt_valid_dev), int(gt_stride), M._mode(mode), _lib.ptr(counts))
+        hw = self.rig.width * self.rig.height
+        return [(M.rates_from_counts(int(c[0]), int(c[1]), int(c[2])), int(c[3]) / hw)
+                for c in counts]
+
 
 @dataclass
 class Sequence:
@@ -339,27 +354,77 @@ def relative_motions(poses):
     return motions
 
 
+def _write_disparity_png(path: str, disp) -> None:
+    """kitti_io.write_disparity_png (kitti_io.py:38-46): 16-bit PNG of
+    round(256 d), 0 = invalid."""
+    import cv2
+    values = disp.values
+    if np.any(disp.valid & (values * 256.0 >= np.iinfo(np.uint16).max + 0.5)):
+        raise ValueError(f"disparity too large for 16-bit encoding in {path}")
+    raw = np.rint(values * 256.0)
+    raw = np.where(disp.valid, np.maximum(raw, 1.0), 0.0).astype(np.uint16)
+    if not cv2.imwrite(path, raw):
+        raise OSError(f"could not write {path}")
+
+
+def _write_color_png(path: str, rgb: np.ndarray) -> None:
+    """kitti_io.write_color_png (kitti_io.py:72-78)."""
+    import cv2
+    if not cv2.imwrite(path, cv2.cvtColor(rgb, cv2.COLOR_RGB2BGR)):
+        raise OSError(f"could not write {path}")
+
+
 def run_sequence(seq: Sequence, params: PipelineParams | None = None, out_dir: str | None = None,
                  metric_mode: str = "or"):
-    """pipeline.py:241-302: per-frame loop plus the metrics lines; the output
-    tree (PNG files) is written only when ``out_dir`` is given and OpenCV is
-    importable."""
+    """Run the pipeline over a sequence, optionally writing an output tree
+    (pipeline.py:241-302): disp_0/ (left fused disparity PNGs), err_0/ (error
+    visualizations, when ground truth is available), metrics.txt (one line
+    per frame) and summary.txt (aggregate key=value pairs).  Bad-pixel counts
+    and error images are computed on the device (metrics.py); PNG encoding
+    stays on the host after the last frame, so it never stalls a step."""
+    from . import metrics
     params = params or PipelineParams()
     pipe = DisparityPipeline(seq.rig, params)
-    results = []
+    results, lines, rates = [], [], []
     for k in range(len(seq)):
-        results.append(pipe.process_frame(seq.lefts[k], seq.rights[k], seq.motions[k]))
+        res = pipe.process_frame(seq.lefts[k], seq.rights[k], seq.motions[k])
+        results.append(res)
+        fl = res.fused.left
+        entry = {
+            "frame": f"{k:06d}",
+            "density": f"{metrics.density(fl):.6f}",
+            "search_fraction": f"{res.search_fraction_left:.6f}",
+        }
+        if seq.gt_left is not None:
+            bad = metrics.bad_pixel_rate(fl, seq.gt_left[k], metric_mode)
+            rates.append(bad.rate)
+            entry["bad_rate"] = f"{bad.rate:.6f}"
+            entry["bad_rate_all"] = f"{bad.rate_all:.6f}"
+            entry["gt_density"] = f"{bad.density:.6f}"
+        lines.append(" ".join(f"{k_}={v}" for k_, v in entry.items()))
     pipe._flush()
+
     if out_dir is not None:
-        import cv2
-        os.makedirs(os.path.join(out_dir, "disp_0"), exist_ok=True)
-        lines = []
+        disp_dir = os.path.join(out_dir, "disp_0")
+        os.makedirs(disp_dir, exist_ok=True)
         for k, res in enumerate(results):
-            fl = res.fused.left
-            raw = np.where(fl.valid, np.maximum(np.rint(fl.values * 256.0), 1.0), 0.0)
-            cv2.imwrite(os.path.join(out_dir, "disp_0", f"{k:06d}.png"), raw.astype(np.uint16))
-            lines.append(f"frame={k:06d} density={float(fl.valid.mean()):.6f} "
-                         f"search_fraction={res.search_fraction_left:.6f}")
+            _write_disparity_png(os.path.join(disp_dir, f"{k:06d}.png"), res.fused.left)
+        if seq.gt_left is not None:
+            err_dir = os.path.join(out_dir, "err_0")
+            os.makedirs(err_dir, exist_ok=True)
+            for k, res in enumerate(results):
+                img = metrics.error_image(res.fused.left, seq.gt_left[k], metric_mode)
+                _write_color_png(os.path.join(err_dir, f"{k:06d}.png"), img)
         with open(os.path.join(out_dir, "metrics.txt"), "w") as fh:
             fh.write("\n".join(lines) + "\n")
+        with open(os.path.join(out_dir, "summary.txt"), "w") as fh:
+            fh.write(f"frames={len(results)}\n")
+            fh.write(f"mode={'baseline' if params.baseline else 'temporal'}\n")
+            fh.write(f"metric_mode={metric_mode}\n")
+            mean_sf = float(np.mean([r.search_fraction_left for r in results]))
+            fh.write(f"mean_search_fraction={mean_sf:.6f}\n")
+            mean_density = float(np.mean([metrics.density(r.fused.left) for r in results]))
+            fh.write(f"mean_density={mean_density:.6f}\n")
+            if seq.gt_left is not None:
+                fh.write(f"mean_bad_rate={float(np.mean(rates)):.6f}\n")
     return results

@@ -122,3 +122,17 @@ def test_sequence_small():
 
 def test_sequence_drive():
     _check_sequence("seq_drive", O.OracleParams(p1=8.0, p2=100.0))
+
+
+def test_metrics():
+    """metrics.py:39-117 restated, against the reference's own outputs
+    (including exact |err| == 3 and |err| == 5 % threshold ties)."""
+    g = load_golden("metrics")
+    for case in range(4):
+        est, ev, gt, gv = (g[f"c{case}_{k}"] for k in ("est", "ev", "gt", "gv"))
+        assert float(ev.mean()) == float(g[f"c{case}_density"])
+        for mode in ("or", "and"):
+            assert np.array_equal(np.array(O.bad_rate(est, ev, gt, gv, mode)),
+                                  g[f"c{case}_{mode}_rates"]), (case, mode)
+            assert np.array_equal(O.bad_mask(est, ev, gt, gv, mode), g[f"c{case}_{mode}_mask"])
+            assert np.array_equal(O.error_rgb(est, ev, gt, gv, mode), g[f"c{case}_{mode}_rgb"])

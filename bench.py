@@ -325,6 +325,20 @@ def main():
     frames_total = B * K * world
     value = frames_total / (ms_max / 1e3)
 
+    # ---- quality (untimed): fused left maps of the last timed frame against
+    # the renderer's ground truth, evaluated on the device (metrics.py)
+    quality = None
+    if rank == 0:
+        _, gts = render_frames(specs, [Wm + K - 1], device, with_gt=True)
+        gt = gts[0][:, 0].contiguous()
+        gv = (gt > 0).to(torch.uint8).contiguous()
+        q = bp.metrics(gt.data_ptr(), gv.data_ptr(), H * W, view=0, mode="or")
+        quality = {"frame": Wm + K - 1, "metric_mode": "or",
+                   "bad_rate": float(np.mean([r.rate for r, _ in q])),
+                   "bad_rate_all": float(np.mean([r.rate_all for r, _ in q])),
+                   "density": float(np.mean([d for _, d in q]))}
+        del gts, gt, gv
+
     # ---- end-to-end through the public API with host buffers ------------
     e2e = None
     if not args.no_e2e:
@@ -392,6 +406,7 @@ def main():
         "pipeline_roofline": {"achieved": frame_bytes / (ms_max / K / 1e3) / 1e9,
                               "frac": frame_bytes / (ms_max / K / 1e3) / 1e9 / peak},
         "gpu_launches": KERNELS_PER_STEP * K,
+        "quality": quality,
         "clocks": clk,
         "e2e": e2e,
     }

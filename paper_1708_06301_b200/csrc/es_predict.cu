@@ -149,9 +149,12 @@ __global__ void k_resolve_fill_h(PredArgs a) {
 }
 
 // vertical pass (axis=0) + final predicted maps + search intervals + the
-// row-ragged pair offsets.  One CTA per image row.
+// row-ragged pair offsets.  One CTA per image row: pass 1 visits the row's
+// pixels at a stride of NT (coalesced loads / stores) and keeps each pixel's
+// slot count in shared memory; pass 2 scans contiguous chunks of the row.
 template <int NT>
 __global__ void __launch_bounds__(NT) k_fill_v_intervals(PredArgs a) {
+  extern __shared__ uint16_t slots[];   // [W]
   __shared__ uint32_t scan_smem[32];
   __shared__ unsigned long long cells_smem;
   const int sv = blockIdx.y;
@@ -160,15 +163,12 @@ __global__ void __launch_bounds__(NT) k_fill_v_intervals(PredArgs a) {
   const int W = a.rig.W, H = a.rig.H, d_max = a.rig.d_max;
   const size_t HW = (size_t)W * H;
   const bool pred = a.have_pred[s] != 0;
-  const int per = (W + NT - 1) / NT;
-  const int x0 = threadIdx.x * per;
-  const int x1 = min(x0 + per, W);
   if (threadIdx.x == 0) cells_smem = 0ull;
-  // pass 1: final predicted values, intervals, this thread's pair count
-  uint32_t my_pairs = 0;
-  unsigned long long my_cells = 0;
-  for (int x = x0; x < x1; ++x) {
-    const size_t i = sv * HW + (size_t)y * W + x;
+  // pass 1: final predicted values, intervals, slot counts
+  uint32_t my_cells = 0;
+  const size_t row = sv * HW + (size_t)y * W;
+  for (int x = threadIdx.x; x < W; x += NT) {
+    const size_t i = row + x;
     double d = 0.0, p = 0.0;
     bool v = false;
     if (pred) {
@@ -191,23 +191,28 @@ __global__ void __launch_bounds__(NT) k_fill_v_intervals(PredArgs a) {
     a.pv[i] = v;
     int lo, hi;
     interval_of(d, p, v, d_max, lo, hi);
-    my_pairs += pixel_slots(lo, hi);
-    my_cells += (unsigned long long)(hi - lo + 1);
+    slots[x] = (uint16_t)pixel_slots(lo, hi);
+    my_cells += (uint32_t)(hi - lo + 1);
     a.meta[i].x = (uint32_t)lo | ((uint32_t)hi << 16);
   }
+  my_cells = __reduce_add_sync(0xffffffffu, my_cells);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&cells_smem, (unsigned long long)my_cells);
+  __syncthreads();
+  // pass 2: offsets (first pair at a 4-aligned slot offset + (j0 & 3))
+  const int per = (W + NT - 1) / NT;
+  const int x0 = min((int)threadIdx.x * per, W);
+  const int x1 = min(x0 + per, W);
+  uint32_t my_pairs = 0;
+  for (int x = x0; x < x1; ++x) my_pairs += slots[x];
   uint32_t total;
   uint32_t base = block_exclusive_scan<NT>(my_pairs, scan_smem, total);
-  // pass 2: offsets (first pair at a 4-aligned slot offset + (j0 & 3))
   const uint32_t rowbase = (uint32_t)(y * row_capacity(W, d_max));
   for (int x = x0; x < x1; ++x) {
-    const size_t i = sv * HW + (size_t)y * W + x;
-    const uint32_t m = a.meta[i].x;
-    const int lo = m & 0xFFFFu, hi = m >> 16;
+    const size_t i = row + x;
+    const int lo = a.meta[i].x & 0xFFFFu;
     a.meta[i].y = rowbase + base + pad_before(lo);
-    base += pixel_slots(lo, hi);
+    base += slots[x];
   }
-  atomicAdd(&cells_smem, my_cells);
-  __syncthreads();
   if (threadIdx.x == 0) {
     atomicAdd(a.cells + sv, cells_smem);
     if (a.cells_acc) atomicAdd(a.cells_acc, cells_smem);
@@ -266,7 +271,7 @@ void launch_predict(const PredArgs& a, int n_sv, cudaStream_t st) {
 
 void launch_fill_v_intervals(const PredArgs& a, int n_sv, cudaStream_t st) {
   cudaMemsetAsync(a.cells, 0, sizeof(unsigned long long) * n_sv, st);
-  k_fill_v_intervals<256><<<dim3(a.rig.H, n_sv), 256, 0, st>>>(a);
+  k_fill_v_intervals<256><<<dim3(a.rig.H, n_sv), 256, sizeof(uint16_t) * a.rig.W, st>>>(a);
 }
 
 void launch_meta_from_intervals(const int64_t* lo, const int64_t* hi, int W, int H, int d_max,

@@ -85,6 +85,71 @@ __global__ void k_warp_zmax(PredArgs a) {
   a.wd[sv * HW + i] = dp;
 }
 
+// k_warp_zmax on 32x8 pixel tiles: the tile's (32+2r)x(8+2r) neighbourhood
+// of d and valid is staged in shared memory once, so the edge test
+// (prediction.py:50-64) reads its window on chip instead of 9 global loads
+// per pixel (r <= ZT_RMAX)
+constexpr int ZT_W = 32, ZT_H = 8, ZT_RMAX = 2;
+
+__global__ void __launch_bounds__(ZT_W * ZT_H) k_warp_zmax_tile(PredArgs a) {
+  __shared__ double td[(ZT_H + 2 * ZT_RMAX) * (ZT_W + 2 * ZT_RMAX)];
+  __shared__ uint8_t tv[(ZT_H + 2 * ZT_RMAX) * (ZT_W + 2 * ZT_RMAX)];
+  const int sv = blockIdx.z;
+  const int s = sv >> 1;
+  if (!a.have_pred[s]) return;
+  const int W = a.rig.W, H = a.rig.H;
+  const size_t HW = (size_t)W * H;
+  const int r = a.prm.edge_reject ? a.prm.edge_window : 0;
+  const int TW = ZT_W + 2 * r, TH = ZT_H + 2 * r;
+  const int bx = blockIdx.x * ZT_W, by = blockIdx.y * ZT_H;
+  const double* d = a.sd + sv * HW;
+  const uint8_t* v = a.sv + sv * HW;
+  const int tid = threadIdx.y * ZT_W + threadIdx.x;
+  for (int k = tid; k < TW * TH; k += ZT_W * ZT_H) {
+    const int xx = bx - r + k % TW, yy = by - r + k / TW;
+    const bool in = xx >= 0 && xx < W && yy >= 0 && yy < H;
+    const size_t g = (size_t)yy * W + xx;
+    tv[k] = in ? v[g] : 0;
+    td[k] = in ? d[g] : 0.0;
+  }
+  __syncthreads();
+  const int x = bx + threadIdx.x, y = by + threadIdx.y;
+  if (x >= W || y >= H) return;
+  const int i = y * W + x;
+  const int c = (threadIdx.y + r) * TW + threadIdx.x + r;
+  uint32_t tgt = NO_SRC;
+  double dp = 0.0;
+  if (tv[c]) {
+    bool edge = false;
+    if (a.prm.edge_reject) {
+      // off-image neighbours are ignored (cval = -+inf), invalid ones too
+      double hi = -INFINITY, lo = INFINITY;
+      for (int oy = -r; oy <= r; ++oy)
+        for (int ox = -r; ox <= r; ++ox) {
+          const int k = c + oy * TW + ox;
+          if (tv[k]) {
+            hi = fmax(hi, td[k]);
+            lo = fmin(lo, td[k]);
+          }
+        }
+      edge = (hi - lo) > a.prm.gamma_e;
+    }
+    if (!edge) {
+      bool at_inf;
+      const double di = td[c];
+      if (warp_src(a.Hm + 16 * sv, a.rig, x, y, di, tgt, dp, at_inf)) {
+        if (!(di > 0.0)) atomicOr(a.err + s, ERR_NONPOSITIVE_D);
+        atomicMax(a.zkey + sv * HW + tgt, (unsigned long long)__double_as_longlong(dp));
+      } else {
+        tgt = NO_SRC;
+        if (at_inf) atomicOr(a.err + s, ERR_POINT_AT_INFINITY);
+      }
+    }
+  }
+  a.wt[sv * HW + i] = tgt;
+  a.wd[sv * HW + i] = dp;
+}
+
 __global__ void k_warp_zidx(PredArgs a) {
   const int sv = blockIdx.y;
   const int s = sv >> 1;
@@ -264,7 +329,12 @@ void launch_predict(const PredArgs& a, int n_sv, cudaStream_t st) {
   dim3 grid((HW + 255) / 256, n_sv);
   cudaMemsetAsync(a.zkey, 0, sizeof(unsigned long long) * (size_t)HW * n_sv, st);
   cudaMemsetAsync(a.zidx, 0xFF, sizeof(uint32_t) * (size_t)HW * n_sv, st);
-  k_warp_zmax<<<grid, 256, 0, st>>>(a);
+  if (!a.prm.edge_reject || a.prm.edge_window <= ZT_RMAX) {
+    dim3 tg((a.rig.W + ZT_W - 1) / ZT_W, (a.rig.H + ZT_H - 1) / ZT_H, n_sv);
+    k_warp_zmax_tile<<<tg, dim3(ZT_W, ZT_H), 0, st>>>(a);
+  } else {
+    k_warp_zmax<<<grid, 256, 0, st>>>(a);
+  }
   k_warp_zidx<<<grid, 256, 0, st>>>(a);
   k_resolve_fill_h<<<grid, 256, 0, st>>>(a);
 }

@@ -1354,6 +1354,13 @@ static void launch_family(const SgmArgs& a, int nch, int fam, int sweeps, int in
   }
 }
 
+static void launch_grp4_g(int G, const SgmArgs& a, int fam, int init, int n_sv, cudaStream_t st) {
+  if (G <= 4) launch_grp4<4, 4, 4>(a, fam, init, n_sv, st);
+  else if (G == 8) launch_grp4<8, 4, 1>(a, fam, init, n_sv, st);
+  else if (G == 16) launch_grp4<16, 4, 1>(a, fam, init, n_sv, st);
+  else launch_grp4<32, 4, 1>(a, fam, init, n_sv, st);
+}
+
 // u16 aggregation with the per-(seq, view) kernel choice: sequences with
 // reduced intervals run the v4 kernel on st_lo, wide ones the 2-pairs/lane
 // kernel on st_hi; each (seq, view) is handled by exactly one stream, so the
@@ -1374,24 +1381,15 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
       lo.S = S[p];
       hi.S = S[p];
       const int init = k < parts;
-      if (np <= 64) {
-        if (g4 == 2) {
-          launch_grp4<4, 2, 4>(lo, fams[k], init, n_sv, st_lo[p]);
-          launch_grp4<8, 2, 1>(hi, fams[k], init, n_sv, st_hi[p]);
-        } else if (g4 == 3) {
-          launch_grp4<8, 4, 1>(lo, fams[k], init, n_sv, st_lo[p]);
-          launch_grp4<8, 4, 1>(hi, fams[k], init, n_sv, st_hi[p]);
-        } else if (g4 == 4) {
-          launch_grp4<4, 4, 3>(lo, fams[k], init, n_sv, st_lo[p]);
-          launch_grp4<8, 4, 1>(hi, fams[k], init, n_sv, st_hi[p]);
-        } else {
-          launch_grp4<4, 4, 4>(lo, fams[k], init, n_sv, st_lo[p]);
-          launch_grp4<8, 4, 1>(hi, fams[k], init, n_sv, st_hi[p]);
-        }
-      } else {
-        launch_grp4<8, 4, 1>(lo, fams[k], init, n_sv, st_lo[p]);
-        launch_grp4<16, 4, 1>(hi, fams[k], init, n_sv, st_hi[p]);
-      }
+      // lanes per chain: G = 4 (8 chains per warp) fills the GPU from ~16
+      // views up; smaller batches widen each chain so that enough warps are
+      // in flight, and D = 256 doubles G so the register-resident chunk
+      // arrays stay at <= 4 words x 4 chunks (measured)
+      static const int widen_env = getenv("ES_SGM_WIDEN") ? atoi(getenv("ES_SGM_WIDEN")) : -1;
+      int widen = widen_env >= 0 ? widen_env : (n_sv <= 2 ? 2 : (n_sv <= 8 ? 1 : 0));
+      if (np > 64) widen += 1;
+      launch_grp4_g(4 << widen, lo, fams[k], init, n_sv, st_lo[p]);
+      launch_grp4_g(8 << widen, hi, fams[k], init, n_sv, st_hi[p]);
     }
     return;
   }
@@ -1428,10 +1426,8 @@ void launch_aggregate(const SgmArgs& a, int arith, int n_sv, cudaStream_t st) {
   static const int g4 = getenv("ES_SGM_G4") ? atoi(getenv("ES_SGM_G4")) : 1;   // A/B switch
   if (arith == ARITH_U16 && !v1 && g4 && !a.lanes) {
     const int fams[4] = {FAM_H, FAM_V, FAM_D1, FAM_D2};
-    for (int k = 0; k < 4; ++k) {
-      if (npairs_max(a.d_max) <= 64) launch_grp4<4, 4, 4>(a, fams[k], k == 0, n_sv, st);
-      else launch_grp4<8, 4, 1>(a, fams[k], k == 0, n_sv, st);
-    }
+    const int widen = (n_sv <= 2 ? 2 : (n_sv <= 8 ? 1 : 0)) + (npairs_max(a.d_max) > 64);
+    for (int k = 0; k < 4; ++k) launch_grp4_g(4 << widen, a, fams[k], k == 0, n_sv, st);
   } else if (arith == ARITH_U16 && !v1) {
     launch_family_seg(a, FAM_H, 3, 1, n_sv, st);
     launch_family_seg(a, FAM_V, 3, 0, n_sv, st);

@@ -8,7 +8,9 @@ there is no CPU fallback.
 
 Modules: core (boundary types), geometry (4x4 homographies, device warp),
 prediction, sgm, fusion (drop-in stage functions), pipeline
-(DisparityPipeline / BatchedPipeline on device-resident state), scenes
+(DisparityPipeline / BatchedPipeline on device-resident state, run_sequence,
+load_sequence), metrics (device bad-pixel evaluation), kitti_io (KITTI-layout
+files), scenes
 (seeded benchmark inputs), build (nvcc build of libegostereo_b200.so).
 """
 
@@ -18,20 +20,21 @@ from .errors import (BehindCameraError, DeviceUnavailableError, DeviceUnsupporte
                      PointAtInfinityError)
 from .fusion import FusionParams, fuse_maps
 from .geometry import disparity_homography, euclidean_warp_oracle, warp_point
-from .metrics import search_space_fraction
+from .metrics import BadPixelResult, bad_pixel_rate, search_space_fraction
 from .pipeline import (BatchedPipeline, DisparityPipeline, FrameResult, PipelineParams,
-                       Sequence, run_sequence)
+                       Sequence, load_sequence, run_sequence, write_sequence)
 from .prediction import PredictionParams, predict_maps
 from .sgm import IntervalMap, SgmParams, full_range_intervals, search_intervals
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "BatchedPipeline", "BehindCameraError", "DeviceUnavailableError", "DeviceUnsupportedError",
+    "BadPixelResult", "BatchedPipeline", "BehindCameraError", "DeviceUnavailableError", "DeviceUnsupportedError",
     "DisparityMap", "DisparityPipeline", "FilterState", "FrameResult", "FusionParams",
     "GrayImage", "IntervalMap", "PipelineParams", "PointAtInfinityError", "PredictionParams",
     "Sequence", "SgmParams", "StereoRig", "VarianceMap", "disparity_homography",
     "euclidean_warp_oracle", "full_range_intervals", "fuse_maps", "make_empty_state",
     "make_invalid_map", "make_motion", "predict_maps", "run_sequence", "search_intervals",
+    "bad_pixel_rate", "load_sequence", "write_sequence",
     "search_space_fraction", "warp_point", "__version__",
 ]

@@ -354,24 +354,65 @@ def relative_motions(poses):
     return motions
 
 
-def _write_disparity_png(path: str, disp) -> None:
-    """kitti_io.write_disparity_png (kitti_io.py:38-46): 16-bit PNG of
-    round(256 d), 0 = invalid."""
-    import cv2
-    values = disp.values
-    if np.any(disp.valid & (values * 256.0 >= np.iinfo(np.uint16).max + 0.5)):
-        raise ValueError(f"disparity too large for 16-bit encoding in {path}")
-    raw = np.rint(values * 256.0)
-    raw = np.where(disp.valid, np.maximum(raw, 1.0), 0.0).astype(np.uint16)
-    if not cv2.imwrite(path, raw):
-        raise OSError(f"could not write {path}")
+def _frame_files(directory: str) -> list:
+    from . import kitti_io
+    names = sorted(n for n in os.listdir(directory) if n.endswith(".png"))
+    if not names:
+        raise kitti_io.FileFormatError(f"{directory}: no PNG frames found")
+    return [os.path.join(directory, n) for n in names]
 
 
-def _write_color_png(path: str, rgb: np.ndarray) -> None:
-    """kitti_io.write_color_png (kitti_io.py:72-78)."""
-    import cv2
-    if not cv2.imwrite(path, cv2.cvtColor(rgb, cv2.COLOR_RGB2BGR)):
-        raise OSError(f"could not write {path}")
+def load_sequence(root: str, d_max: int) -> Sequence:
+    """Read a KITTI-layout sequence directory (pipeline.py:203-238): calib.txt,
+    poses.txt, image_0/ and image_1/ PNG frames, optional gt_disp_0/1."""
+    from . import kitti_io
+    calib = kitti_io.read_calib_file(os.path.join(root, "calib.txt"))
+    lf = _frame_files(os.path.join(root, "image_0"))
+    rf = _frame_files(os.path.join(root, "image_1"))
+    if len(lf) != len(rf):
+        raise kitti_io.FileFormatError(
+            f"{root}: image_0 has {len(lf)} frames, image_1 has {len(rf)}")
+    lefts = [kitti_io.read_gray_png(f) for f in lf]
+    rights = [kitti_io.read_gray_png(f) for f in rf]
+    h, w = lefts[0].data.shape
+    if any(img.data.shape != (h, w) for img in lefts + rights):
+        raise kitti_io.FileFormatError(f"{root}: frame dimensions are not uniform")
+    rig = StereoRig(f=calib.f, b=calib.b, cx=calib.cx, cy=calib.cy, width=w, height=h,
+                    d_max=d_max)
+    poses = kitti_io.read_pose_file(os.path.join(root, "poses.txt"))
+    if len(poses) != len(lefts):
+        raise kitti_io.FileFormatError(f"{root}: {len(poses)} poses for {len(lefts)} frames")
+    seq = Sequence(rig, lefts, rights, relative_motions(poses))
+    for attr, sub in (("gt_left", "gt_disp_0"), ("gt_right", "gt_disp_1")):
+        gt_dir = os.path.join(root, sub)
+        if os.path.isdir(gt_dir):
+            files = _frame_files(gt_dir)
+            if len(files) != len(lefts):
+                raise kitti_io.FileFormatError(
+                    f"{root}: {len(files)} maps in {sub} for {len(lefts)} frames")
+            setattr(seq, attr, [kitti_io.read_disparity_png(f) for f in files])
+    return seq
+
+
+def write_sequence(root: str, seq: Sequence, poses) -> None:
+    """Materialise an in-memory sequence as a KITTI-layout directory
+    (pipeline.py:305-322)."""
+    from . import kitti_io
+    kitti_io.ensure_dir(root)
+    kitti_io.write_calib_file(os.path.join(root, "calib.txt"),
+                              kitti_io.CalibData(f=seq.rig.f, cx=seq.rig.cx, cy=seq.rig.cy,
+                                                 b=seq.rig.b))
+    kitti_io.write_pose_file(os.path.join(root, "poses.txt"), poses)
+    for sub, images in (("image_0", seq.lefts), ("image_1", seq.rights)):
+        d = kitti_io.ensure_dir(os.path.join(root, sub))
+        for k, img in enumerate(images):
+            kitti_io.write_gray_png(os.path.join(d, f"{k:06d}.png"), img)
+    for sub, maps in (("gt_disp_0", seq.gt_left), ("gt_disp_1", seq.gt_right)):
+        if maps is None:
+            continue
+        d = kitti_io.ensure_dir(os.path.join(root, sub))
+        for k, m in enumerate(maps):
+            kitti_io.write_disparity_png(os.path.join(d, f"{k:06d}.png"), m)
 
 
 def run_sequence(seq: Sequence, params: PipelineParams | None = None, out_dir: str | None = None,
@@ -382,7 +423,7 @@ def run_sequence(seq: Sequence, params: PipelineParams | None = None, out_dir: s
     per frame) and summary.txt (aggregate key=value pairs).  Bad-pixel counts
     and error images are computed on the device (metrics.py); PNG encoding
     stays on the host after the last frame, so it never stalls a step."""
-    from . import metrics
+    from . import kitti_io, metrics
     params = params or PipelineParams()
     pipe = DisparityPipeline(seq.rig, params)
     results, lines, rates = [], [], []
@@ -408,13 +449,13 @@ def run_sequence(seq: Sequence, params: PipelineParams | None = None, out_dir: s
         disp_dir = os.path.join(out_dir, "disp_0")
         os.makedirs(disp_dir, exist_ok=True)
         for k, res in enumerate(results):
-            _write_disparity_png(os.path.join(disp_dir, f"{k:06d}.png"), res.fused.left)
+            kitti_io.write_disparity_png(os.path.join(disp_dir, f"{k:06d}.png"), res.fused.left)
         if seq.gt_left is not None:
             err_dir = os.path.join(out_dir, "err_0")
             os.makedirs(err_dir, exist_ok=True)
             for k, res in enumerate(results):
                 img = metrics.error_image(res.fused.left, seq.gt_left[k], metric_mode)
-                _write_color_png(os.path.join(err_dir, f"{k:06d}.png"), img)
+                kitti_io.write_color_png(os.path.join(err_dir, f"{k:06d}.png"), img)
         with open(os.path.join(out_dir, "metrics.txt"), "w") as fh:
             fh.write("\n".join(lines) + "\n")
         with open(os.path.join(out_dir, "summary.txt"), "w") as fh:

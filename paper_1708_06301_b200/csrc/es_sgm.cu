@@ -1704,47 +1704,56 @@ __global__ void __launch_bounds__(WR_WARPS * 32) k_wta_runs(WtaArgs a, int rmax)
     for (int j = 0; j < nrun; ++j) tab[excl + j] = (uint8_t)lane;
     key[lane] = 0xFFFFFFFFu;
     __syncwarp();
-    for (int r0 = 0; r0 < total; r0 += 32) {
-      const int r = r0 + lane;
-      const bool live = r < total;
-      const int p = live ? tab[r] : 31;
-      const int plo = __shfl_sync(FULL, lo, p);
-      const int phi = __shfl_sync(FULL, hi, p);
-      const int pex = __shfl_sync(FULL, excl, p);
-      const uint32_t prun = __shfl_sync(FULL, run0, p);
-      uint32_t best = 0xFFFFFFFFu;
-      if (live) {
-        const int j = r - pex;
-        uint4 w = Sv[0][prun + j];
+    // two runs per lane per iteration: all partial-sum loads of both are in
+    // flight before either is reduced; keys go to the pixel's slot with a
+    // shared-memory atomicMin (ties resolve to the smaller d by the key)
+    for (int r0 = 0; r0 < total; r0 += 64) {
+      int p[2], plo[2], phi[2], pex[2];
+      uint32_t prun[2];
+      bool live[2];
+      uint4 w[2];
 #pragma unroll
-        for (int i = 1; i < N; ++i) {
-          const uint4 v = Sv[i][prun + j];
-          w = make_uint4(__vadd2(w.x, v.x), __vadd2(w.y, v.y), __vadd2(w.z, v.z), __vadd2(w.w, v.w));
+      for (int u = 0; u < 2; ++u) {
+        const int r = r0 + 32 * u + lane;
+        live[u] = r < total;
+        p[u] = live[u] ? tab[r] : 31;
+        plo[u] = __shfl_sync(FULL, lo, p[u]);
+        phi[u] = __shfl_sync(FULL, hi, p[u]);
+        pex[u] = __shfl_sync(FULL, excl, p[u]);
+        prun[u] = __shfl_sync(FULL, run0, p[u]);
+        w[u] = make_uint4(0u, 0u, 0u, 0u);
+        if (live[u]) {
+          const int j = r - pex[u];
+          w[u] = Sv[0][prun[u] + j];
+#pragma unroll
+          for (int i = 1; i < N; ++i) {
+            const uint4 v = Sv[i][prun[u] + j];
+            w[u] = make_uint4(__vadd2(w[u].x, v.x), __vadd2(w[u].y, v.y), __vadd2(w[u].z, v.z),
+                              __vadd2(w[u].w, v.w));
+          }
         }
-        const uint32_t d0 = (uint32_t)((plo & ~7) + 8 * j);
-        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!live[u]) continue;
+        const int j = r0 + 32 * u + lane - pex[u];
+        const uint32_t d0 = (uint32_t)((plo[u] & ~7) + 8 * j);
+        const uint32_t ww[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
         uint32_t k[8];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           k[2 * q] = (ww[q] << 16) | (d0 + 2 * q);
           k[2 * q + 1] = (ww[q] & 0xFFFF0000u) | (d0 + 2 * q + 1);
         }
-        if ((int)d0 < plo || (int)d0 + 7 > phi) {
+        if ((int)d0 < plo[u] || (int)d0 + 7 > phi[u]) {
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            if ((int)d0 + i < plo || (int)d0 + i > phi) k[i] = 0xFFFFFFFFu;
+            if ((int)d0 + i < plo[u] || (int)d0 + i > phi[u]) k[i] = 0xFFFFFFFFu;
         }
-        best = min(min(min(k[0], k[1]), min(k[2], k[3])), min(min(k[4], k[5]), min(k[6], k[7])));
+        const uint32_t best =
+            min(min(min(k[0], k[1]), min(k[2], k[3])), min(min(k[4], k[5]), min(k[6], k[7])));
+        atomicMin(&key[p[u]], best);
       }
-      // segmented minimum over the lanes of one pixel (contiguous lanes)
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t ob = __shfl_down_sync(FULL, best, o);
-        const int op = __shfl_down_sync(FULL, p, o);
-        if (lane + o < 32 && op == p) best = min(best, ob);
-      }
-      const int pp = __shfl_up_sync(FULL, p, 1);
-      if (live && (lane == 0 || pp != p)) atomicMin(&key[p], best);
     }
     __syncwarp();
     if (pix < HW) {

@@ -189,31 +189,47 @@ class Clocks:
 
 def _cpu_worker(args):
     # spawned: the module globals are config 5's, so the rig travels with the job
-    left0, right0, left1, right1, motion, rig = args
+    frames, motions, rig = args
     import oracle as O
     orc = O.OracleStereo(rig["f"], rig["b"], rig["cx"], rig["cy"], rig["width"], rig["height"],
                          rig["d_max"])
-    orc.step(left0, right0, None)
+    orc.step(frames[0][0], frames[0][1], None)          # full-range frame 0: warm-up
     t0 = time.perf_counter()
-    orc.step(left1, right1, motion)
+    for k in range(1, len(frames)):
+        orc.step(frames[k][0], frames[k][1], motions[k])
     return time.perf_counter() - t0
 
 
-def cpu_baseline(imgs0, imgs1, motions, procs):
-    """numpy oracle port: P processes, each one full-range warm frame (not
-    timed) then one timed predicted frame of its own sequence."""
-    P = min(procs, len(motions))
-    jobs = [(imgs0[s, 0], imgs0[s, 1], imgs1[s, 0], imgs1[s, 1], motions[s], RIG)
-            for s in range(P)]
+def default_cpu_procs():
+    """Every host core the process may use, bounded by memory (the numpy
+    port needs ~1.1 GB per 1242x375 frame step)."""
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    try:
+        mem_gb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2**30
+        cores = max(1, min(cores, int(mem_gb / 1.5)))
+    except (ValueError, OSError, AttributeError):
+        pass
+    return cores
+
+
+def cpu_baseline(imgs, specs, procs, n_timed=1):
+    """numpy oracle port: P single-threaded processes, each its own sequence:
+    one full-range warm-up frame (not timed) then ``n_timed`` predicted
+    frames; frames/s = P * n_timed / slowest process."""
+    P = min(procs, len(specs))
+    jobs = [([(imgs[k, s, 0], imgs[k, s, 1]) for k in range(n_timed + 1)],
+             [motions_for(specs, k)[s] for k in range(n_timed + 1)], RIG) for s in range(P)]
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     t0 = time.perf_counter()
     with mp.get_context("spawn").Pool(P) as pool:
         per = pool.map(_cpu_worker, jobs)
     wall = time.perf_counter() - t0
-    fps = P / max(per)
+    fps = P * n_timed / max(per)
     return {"value": fps, "unit": "frames/s", "cores": P, "kind": "port",
-            "sample": f"{P} sequences x 1 predicted frame ({W}x{H}, D={D_MAX + 1}) in {P} parallel "
-                      f"processes; per-frame {min(per):.1f}-{max(per):.1f} s; wall {wall:.0f} s "
-                      "incl. the untimed full-range frame"}
+            "sample": f"{P} sequences x {n_timed} predicted frame(s) ({W}x{H}, D={D_MAX + 1}) in "
+                      f"{P} parallel single-threaded processes; per-process {min(per):.1f}-"
+                      f"{max(per):.1f} s; wall {wall:.0f} s incl. the untimed full-range frame"}
 
 
 # ----------------------------------------------------------------- main
@@ -229,7 +245,7 @@ def main():
     ap.add_argument("--batch", type=int, default=None,
                     help="sequences per GPU (default: config 5: 64, config 4: 8)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-procs", type=int, default=min(8, os.cpu_count() or 1))
+    ap.add_argument("--cpu-procs", type=int, default=default_cpu_procs())
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--texture-scale", type=float, default=TEXTURE_SCALE,
@@ -263,10 +279,12 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
+        # each timed step = one predicted frame of every process's sequence
         specs = sequence_specs(args.cpu_procs, seed0=5000)
-        imgs = render_frames(specs, [0, 1], device).cpu().numpy()
-        motions = motions_for(specs, 1)
-        cb = cpu_baseline(imgs[0], imgs[1], motions, args.cpu_procs)
+        # (config 4: one predicted frame -- a 2048x1024 D=256 numpy step takes minutes)
+        nt = K if args.config == 5 else 1
+        imgs = render_frames(specs, list(range(nt + 1)), device).cpu().numpy()
+        cb = cpu_baseline(imgs, specs, args.cpu_procs, n_timed=nt)
         print(json.dumps({
             "impl": "reference", "metric": "frames/s", "value": cb["value"], "unit": "frames/s",
             "n_gpus": args.gpus, "steps": K, "warmup": Wm, "higher_is_better": True,
@@ -413,8 +431,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         specs_c = sequence_specs(args.cpu_procs, seed0=1000)
         imgs_c = render_frames(specs_c, [0, 1], device).cpu().numpy()
-        line["cpu_baseline"] = cpu_baseline(imgs_c[0], imgs_c[1], motions_for(specs_c, 1),
-                                            args.cpu_procs)
+        line["cpu_baseline"] = cpu_baseline(imgs_c, specs_c, args.cpu_procs, n_timed=1)
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

@@ -22,6 +22,7 @@
 //     operation order, 8 single-direction launches in the reference's
 //     summation order (H->, H<-, dy=+1 dx=-1,0,1, dy=-1 dx=-1,0,1).
 #include <cstdlib>
+#include <type_traits>
 
 #include "es_common.cuh"
 #include "es_kernels.h"
@@ -889,6 +890,12 @@ template <int PPL>
 struct Vec;
 template <>
 struct Vec<2> {
+  __device__ static __forceinline__ void ld_any(const uint32_t* p, bool pred, uint32_t* o) {
+    uint32_t a, b;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q ld.global.v2.u32 {%0, %1}, [%2];\n\t}\n"
+                 : "=r"(a), "=r"(b) : "l"(p), "r"((int)pred));
+    o[0] = a; o[1] = b;
+  }
   __device__ static __forceinline__ void ldc(const uint32_t* p, bool pred, uint32_t* o) {
     uint32_t a = INF16x2, b = INF16x2;
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q ld.global.nc.v2.u32 {%0, %1}, [%2];\n\t}\n"
@@ -908,6 +915,14 @@ struct Vec<2> {
 };
 template <>
 struct Vec<4> {
+  // predicated load that leaves the registers undefined when off (callers
+  // only use them under the same predicate)
+  __device__ static __forceinline__ void ld_any(const uint32_t* p, bool pred, uint32_t* o) {
+    uint32_t a, b, c, d;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}\n"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p), "r"((int)pred));
+    o[0] = a; o[1] = b; o[2] = c; o[3] = d;
+  }
   __device__ static __forceinline__ void ldc(const uint32_t* p, bool pred, uint32_t* o) {
     uint32_t a = INF16x2, b = INF16x2, c = INF16x2, d = INF16x2;
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}\n"
@@ -958,8 +973,11 @@ __global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int
   auto umask = [](int lo, int hi) -> uint32_t {
     return hi < lo ? 0u : ((hi >= 31 ? 0xFFFFFFFFu : ((2u << hi) - 1u)) & ~((1u << lo) - 1u));
   };
-  for (int bwd = 0; bwd < 2; ++bwd) {
-    const bool load_sum = !(init && bwd == 0);
+  // one specialised body per partial-sum mode: the first family's forward
+  // sweep stores L (no partial-sum load); every other sweep loads the
+  // partial sum only where it stores, so its loads need no default value
+  auto sweep = [&](const int bwd, auto load_sum_tag) {
+    constexpr bool load_sum = decltype(load_sum_tag)::value;
     // chain metadata: every lane loads its chain's pixel itself, four steps
     // ahead, into the register set of the step's parity (no register
     // rotation, so nothing waits on a load before its use)
@@ -989,7 +1007,7 @@ __global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int
     auto fetch = [&](const G4Step& s, uint32_t (&cn)[NW], uint32_t (&sn)[NW], int c) {
       const bool p = pred_of(s, c);
       Vec<PPL>::ldc(C + s.base + c * CW, p, &cn[c * PPL]);
-      Vec<PPL>::ld(S + s.base + c * CW, p && load_sum, &sn[c * PPL]);
+      if constexpr (load_sum) Vec<PPL>::ld_any(S + s.base + c * CW, p, &sn[c * PPL]);
     };
     uint32_t prev[NW], cA[NW], sA[NW], cB[NW], sB[NW];
     uint2 mA = load_meta(0), mB = load_meta(1);
@@ -1031,7 +1049,7 @@ __global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int
             // L = C + min(Lp(d), Lp(d-1)+P1, Lp(d+1)+P1, m+P2) - m   (sgm.py:205-215)
             const uint32_t cand = __viaddmin_u16x2(__vminu2(X[k], X[k + 1]), p1x2, __vminu2(P[k], mp2));
             L[k] = __vadd2(cn[c * PPL + k], __vadd2(cand, ng));
-            Ssum[k] = __vadd2(sn[c * PPL + k], L[k]);
+            Ssum[k] = load_sum ? __vadd2(sn[c * PPL + k], L[k]) : L[k];
             prev[c * PPL + k] = L[k];
           }
           if (PPL == 4) {
@@ -1069,6 +1087,10 @@ __global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int
       s0 = s2;
       s1 = s3;
     }
+  };
+  for (int bwd = 0; bwd < 2; ++bwd) {
+    if (init && bwd == 0) sweep(bwd, std::false_type{});
+    else sweep(bwd, std::true_type{});
   }
 }
 

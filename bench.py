@@ -378,6 +378,7 @@ def main():
             # sequences out, every step
             bp.process_frames(staged[i].numpy(), motions_for(specs, Wm + i), sync=False)
             bp.fused_kitti(0, out=outs[i].numpy().view(np.uint16), sync=False)
+        bp.fence()   # the last export's device->host copy is inside the timed region
         with torch.cuda.stream(ext):
             e1.record()
         bp.sync()

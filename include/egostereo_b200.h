@@ -75,6 +75,11 @@ int es_ctx_reset(es_ctx* ctx);
 int es_ctx_step(es_ctx* ctx, const uint8_t* images, int images_dev, const double* homographies,
                 const uint8_t* motion_given, int sync);
 int es_ctx_sync(es_ctx* ctx);
+/* make the context's compute stream wait for every host<->device transfer
+ * issued so far (input uploads run on a copy stream, es_ctx_export_all's
+ * KITTI copies on another), so an event recorded on the compute stream
+ * afterwards also covers the last export */
+int es_ctx_fence(es_ctx* ctx);
 /* frame counter of sequence s (FilterState.frame) and searched cells per view */
 int es_ctx_frame(es_ctx* ctx, int seq, int64_t* frame);
 int es_ctx_cells(es_ctx* ctx, int seq, uint64_t* cells_left, uint64_t* cells_right);

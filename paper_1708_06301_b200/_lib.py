@@ -59,6 +59,7 @@ SIGNATURES = {
     "es_ctx_reset": [_P],
     "es_ctx_step": [_P, _P, _I, _P, _P, _I],
     "es_ctx_sync": [_P],
+    "es_ctx_fence": [_P],
     "es_ctx_frame": [_P, _I, _P],
     "es_ctx_cells": [_P, _I, _P, _P],
     "es_ctx_have_state": [_P, _I, _P],

@@ -118,6 +118,18 @@ __global__ void k_kitti(const double* d, const uint8_t* v, size_t n, uint16_t* o
   double raw = rint(d[i] * 256.0);
   o[i] = v[i] ? (uint16_t)fmin(fmax(raw, 1.0), 65535.0) : (uint16_t)0;
 }
+
+// the same for every sequence of a batch: sequence s at d + s * stride
+__global__ void k_kitti_batch(const double* d, const uint8_t* v, size_t n, size_t stride,
+                              uint16_t* o) {
+  const size_t s = blockIdx.y;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double x = d[s * stride + i];
+  const bool ok = v[s * stride + i] != 0;
+  const double raw = rint(x * 256.0);
+  o[s * n + i] = ok ? (uint16_t)fmin(fmax(raw, 1.0), 65535.0) : (uint16_t)0;
+}
 // warp_point on principal-point-relative (x, y, d) triples (geometry.py:95-115)
 __global__ void k_warp_points(const double* Hm, const double* pts, int n, double* out, int* err) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -199,7 +211,17 @@ struct es_ctx {
   static constexpr int NSTAGE = 6;
   bool profiling = false;
   std::vector<std::array<cudaEvent_t, NSTAGE + 1>> prof;
-  uint16_t* kitti = nullptr;   // batched KITTI export staging
+  uint16_t* kitti = nullptr;   // batched KITTI export staging (2 slots)
+  // host<->device copy overlap: input images are double-buffered (img,
+  // img2) and uploaded on cp_in; KITTI exports are copied out on cp_out, so
+  // both transfers overlap the neighbouring steps' kernels
+  uint8_t* img2 = nullptr;
+  uint8_t* img_cur = nullptr;  // buffer the current step's kernels read
+  int img_slot = 0;
+  int kitti_slot = 0;
+  cudaStream_t cp_in = nullptr, cp_out = nullptr;
+  cudaEvent_t ev_img_free[2] = {}, ev_img_ready = nullptr, ev_kitti_ready = nullptr,
+              ev_kitti_free[2] = {};
   unsigned long long* cells_acc = nullptr;   // searched cells summed over steps
   int lanes = 0;               // SGM lanes per chain (0 = heuristic)
   double last_fraction = 1.0;  // search fraction of the last synced step
@@ -221,7 +243,7 @@ int ctx_free(es_ctx* c) {
                   c->C, c->S,
                   c->Sx[0], c->Sx[1], c->Sx[2], c->dstar, c->r, c->mvalid, c->keep, c->Hm,
                   c->have_pred, c->err, c->anyv,
-                  c->cells, c->kitti, c->cells_acc};
+                  c->cells, c->kitti, c->cells_acc, c->img2};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   void* hptrs[] = {c->h_Hm, c->h_have, c->h_err, c->h_anyv, c->h_cells};
@@ -236,6 +258,11 @@ int ctx_free(es_ctx* c) {
     if (s) cudaStreamDestroy(s);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  for (cudaEvent_t e : {c->ev_img_free[0], c->ev_img_free[1], c->ev_img_ready, c->ev_kitti_ready,
+                        c->ev_kitti_free[0], c->ev_kitti_free[1]})
+    if (e) cudaEventDestroy(e);
+  if (c->cp_in) cudaStreamDestroy(c->cp_in);
+  if (c->cp_out) cudaStreamDestroy(c->cp_out);
   delete c;
   return ES_OK;
 }
@@ -306,6 +333,7 @@ int es_ctx_create(int device, const es_rig* rig, const es_params* prm, int batch
   const size_t vol_words = c->volcap * 2 * batch * (c->arith == ARITH_F32 ? 2 : 1);
   int e = ES_OK;
   if (!e) e = dalloc(&c->img, n);
+  if (!e) e = dalloc(&c->img2, n);
   for (int k = 0; k < 2 && !e; ++k) {
     e = dalloc(&c->sd[k], n);
     if (!e) e = dalloc(&c->sp[k], n);
@@ -366,7 +394,15 @@ int es_ctx_create(int device, const es_rig* rig, const es_params* prm, int batch
       cudaStreamCreateWithFlags(&c->sx[5], cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->sx[6], cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->cp_in, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->cp_out, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_img_free[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_img_free[1], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_img_ready, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_kitti_ready, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_kitti_free[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_kitti_free[1], cudaEventDisableTiming) != cudaSuccess) {
     ctx_free(c);
     return fail(ES_ERR_CUDA, "pinned host / stream allocation failed");
   }
@@ -402,6 +438,7 @@ int es_ctx_reset(es_ctx* c) {
 int es_ctx_sync(es_ctx* c) {
   CK(cudaSetDevice(c->device));
   CK(cudaStreamSynchronize(c->st));
+  CK(cudaStreamSynchronize(c->cp_out));
   if (c->pending) {
     c->pending = false;
     for (int s = 0; s < c->B; ++s) c->have_state[s] = c->h_anyv[s] != 0;
@@ -446,11 +483,16 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   auto mark = [&](int k) {
     if (ev) cudaEventRecord(ev[k], c->st);
   };
-  if (images_dev) {
-    CK(cudaMemcpyAsync(c->img, images, HW * 2 * B, cudaMemcpyDeviceToDevice, c->st));
-  } else {
-    CK(cudaMemcpyAsync(c->img, images, HW * 2 * B, cudaMemcpyHostToDevice, c->st));
-  }
+  // this step's images go to the buffer the step before last read; its
+  // upload waits only for that step's cost kernel, not for the previous step
+  const int ib = c->img_slot;
+  c->img_slot ^= 1;
+  c->img_cur = ib ? c->img2 : c->img;
+  CK(cudaStreamWaitEvent(c->cp_in, c->ev_img_free[ib], 0));
+  CK(cudaMemcpyAsync(c->img_cur, images, HW * 2 * B,
+                     images_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->cp_in));
+  CK(cudaEventRecord(c->ev_img_ready, c->cp_in));
+  CK(cudaStreamWaitEvent(c->st, c->ev_img_ready, 0));
   CK(cudaMemcpyAsync(c->Hm, h_Hm, sizeof(double) * 32 * B, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(c->have_pred, h_have, B, cudaMemcpyHostToDevice, c->st));
   CK(cudaEventRecord(c->ring_ev[slot], c->st));
@@ -470,12 +512,13 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   ca.H = c->rig.H;
   ca.d_max = c->rig.d_max;
   ca.window = c->prm.window;
-  ca.img = c->img;
+  ca.img = c->img_cur;
   ca.meta = c->meta;
   ca.C = c->C;
   ca.volcap = c->volcap;
   ca.view0 = 0;
   launch_cost(ca, n_sv, c->st);
+  CK(cudaEventRecord(c->ev_img_free[ib], c->st));   // the images' last reader
   mark(3);
 
   SgmArgs sa;
@@ -743,14 +786,21 @@ extern "C" int es_ctx_export_all(es_ctx* c, int what, int view, void* out, int s
   const size_t HW = c->HW;
   const int B = c->B;
   if (what == ES_FUSED_KITTI) {
-    if (!c->kitti) CK(cudaMalloc(&c->kitti, sizeof(uint16_t) * HW * B));
-    for (int s = 0; s < B; ++s) {
-      const size_t o = ((size_t)s * 2 + view) * HW;
-      k_kitti<<<(unsigned)((HW + 255) / 256), 256, 0, c->st>>>(c->sd[c->cur] + o, c->sv[c->cur] + o,
-                                                               HW, c->kitti + (size_t)s * HW);
-    }
+    // encode on the compute stream into one of two staging slots, copy out
+    // on cp_out: the transfer overlaps the next step's kernels
+    if (!c->kitti) CK(cudaMalloc(&c->kitti, sizeof(uint16_t) * HW * B * 2));
+    const int kb = c->kitti_slot;
+    c->kitti_slot ^= 1;
+    uint16_t* stage = c->kitti + (size_t)kb * HW * B;
+    CK(cudaStreamWaitEvent(c->st, c->ev_kitti_free[kb], 0));
+    k_kitti_batch<<<dim3((unsigned)((HW + 255) / 256), B), 256, 0, c->st>>>(
+        c->sd[c->cur] + (size_t)view * HW, c->sv[c->cur] + (size_t)view * HW, HW, 2 * HW, stage);
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(out, c->kitti, sizeof(uint16_t) * HW * B, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaEventRecord(c->ev_kitti_ready, c->st));
+    CK(cudaStreamWaitEvent(c->cp_out, c->ev_kitti_ready, 0));
+    CK(cudaMemcpyAsync(out, stage, sizeof(uint16_t) * HW * B, cudaMemcpyDeviceToHost, c->cp_out));
+    CK(cudaEventRecord(c->ev_kitti_free[kb], c->cp_out));
+    if (sync) CK(cudaStreamSynchronize(c->cp_out));
   } else {
     void* p;
     if (int e = es_ctx_device_ptr(c, what, 0, view, &p)) return e;
@@ -1260,5 +1310,14 @@ extern "C" int es_ctx_metrics(es_ctx* c, int view, const double* gt_dev, const u
   CK(cudaMemcpyAsync(counts, dc, sizeof(uint64_t) * 4 * c->B, cudaMemcpyDeviceToHost, c->st));
   CK(cudaFreeAsync(dc, c->st));
   CK(cudaStreamSynchronize(c->st));
+  return ES_OK;
+}
+
+// make the compute stream wait for every transfer issued so far (so an event
+// recorded on it afterwards covers the last export's device->host copy)
+extern "C" int es_ctx_fence(es_ctx* c) {
+  CK(cudaSetDevice(c->device));
+  CK(cudaEventRecord(c->ev_join, c->cp_out));
+  CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
   return ES_OK;
 }

@@ -301,6 +301,11 @@ class BatchedPipeline:
     def sync(self):
         self.engine.sync()
 
+    def fence(self):
+        """Order the engine's compute stream after every transfer issued so
+        far (uploads and exports run on their own copy streams)."""
+        _lib.call("es_ctx_fence", self.engine._h)
+
     def fused_kitti(self, view: int = 0, out=None, sync: bool = True) -> np.ndarray:
         """Fused disparity of every sequence in the KITTI uint16 encoding
         (kitti_io.py:38-46), one batched device->host copy.  With

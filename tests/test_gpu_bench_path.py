@@ -59,3 +59,37 @@ def test_batched_deferred_path_matches_oracle():
         enc = np.where(fl[2], np.maximum(np.rint(fl[0] * 256.0), 1.0), 0.0).astype(np.uint16)
         assert np.array_equal(kitti[s], enc), s
         assert got.search_fraction_left < 1.0
+
+
+def test_e2e_host_inputs_async_exports_match_oracle():
+    """The e2e pattern: pinned host images uploaded on the copy stream
+    (double-buffered), deferred steps, one asynchronous KITTI export per step
+    into its own pinned buffer, a fence and one sync at the end -- every
+    step's export must equal that frame's oracle state."""
+    import torch
+    from paper_1708_06301_b200 import pipeline, scenes
+    from paper_1708_06301_b200.core import StereoRig
+    import bench
+    B, n = 3, 5
+    rig = StereoRig(f=180.0, b=0.54, cx=151.0, cy=46.0, width=310, height=94, d_max=40)
+    specs = [scenes.sequence_spec(seed=700 + s, n_frames=n, step=0.5, z_range=(4.0, 30.0))
+             for s in range(B)]
+    imgs = bench.render_frames(specs, list(range(n)), "cuda:0", rig=rig)
+    staged = [imgs[k].cpu().pin_memory() for k in range(n)]
+    outs = [torch.empty((B, rig.height, rig.width), dtype=torch.int16, pin_memory=True)
+            for _ in range(n)]
+    bp = pipeline.BatchedPipeline(rig, B)
+    bp.process_frames(staged[0].numpy(), [sp[2][0] for sp in specs], sync=True)
+    bp.fused_kitti(0, out=outs[0].numpy().view(np.uint16), sync=True)
+    for k in range(1, n):
+        bp.process_frames(staged[k].numpy(), [sp[2][k] for sp in specs], sync=False)
+        bp.fused_kitti(0, out=outs[k].numpy().view(np.uint16), sync=False)
+    bp.fence()
+    bp.sync()
+    host = imgs.cpu().numpy()
+    for s in range(B):
+        orc = O.OracleStereo(rig.f, rig.b, rig.cx, rig.cy, rig.width, rig.height, rig.d_max)
+        for k in range(n):
+            want = orc.step(host[k, s, 0], host[k, s, 1], specs[s][2][k])["left_fused"]
+            enc = np.where(want[2], np.maximum(np.rint(want[0] * 256.0), 1.0), 0.0).astype(np.uint16)
+            assert np.array_equal(outs[k].numpy().view(np.uint16)[s], enc), (s, k)

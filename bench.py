@@ -141,6 +141,11 @@ def render_frames(specs, frames, device, rig=None, with_gt=False):
     return (out, gt) if with_gt else out
 
 
+def motions_for_frames(specs, k0, k1):
+    """Motions of sequence 0's frames k0 .. k1-1 (None for frame 0)."""
+    return [specs[0][2][k % SEQ_FRAMES] for k in range(k0, k1)]
+
+
 def motions_for(specs, k):
     return [sp[2][k % SEQ_FRAMES] for sp in specs]
 

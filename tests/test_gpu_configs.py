@@ -98,3 +98,53 @@ def test_config3_class_moving_boxes_and_salt_noise():
             img[v][mask] = 255
     fr = _compare(rig, frames, motions)
     assert fr[0] == 1.0 and min(fr[1:]) < 1.0
+
+
+@pytest.mark.slow
+def test_config2_full_size_sequence():
+    """BASELINE config 2 at its full size (1242x375, D = 128, f = 718.9,
+    b = 0.54, 1 m/frame with yaw/pitch/roll noise): the bench's device-rendered
+    scene, frame 0 full range then predicted frames, bit-exact vs the oracle."""
+    import bench
+    from paper_1708_06301_b200 import core
+    rig = core.StereoRig(**bench.RIG)
+    specs = bench.sequence_specs(1, seed0=2000)
+    imgs = bench.render_frames(specs, [0, 1, 2], "cuda:0").cpu().numpy()
+    frames = [imgs[k, 0] for k in range(3)]
+    fr = _compare(rig, frames, bench.motions_for_frames(specs, 0, 3))
+    assert fr[0] == 1.0 and fr[2] < 1.0
+
+
+@pytest.mark.slow
+def test_config4_full_size_batched_equals_single():
+    """BASELINE config 4 at its full size (2048x1024, D = 256): two sequences
+    in one batched context give exactly the maps each gives alone (the
+    batched launch geometry, the D = 256 kernels and the partial sums are
+    per-(sequence, view) independent)."""
+    import bench
+    from paper_1708_06301_b200 import core, pipeline
+    bench.use_config(4)
+    try:
+        rig = core.StereoRig(**bench.RIG)
+        specs = bench.sequence_specs(2, seed0=4000)
+        imgs = bench.render_frames(specs, [0, 1, 2], "cuda:0")
+        bp = pipeline.BatchedPipeline(rig, 2)
+        singles = [pipeline.DisparityPipeline(rig) for _ in range(2)]
+        host = imgs.cpu().numpy()
+        for k in range(3):
+            bp.process_frames(None, bench.motions_for(specs, k), sync=True,
+                              images_dev=imgs[k].data_ptr())
+            for s in range(2):
+                res = singles[s].process_frame(core.GrayImage(host[k, s, 0]),
+                                               core.GrayImage(host[k, s, 1]),
+                                               bench.motions_for(specs, k)[s])
+                got = bp.result(s)
+                for a, b in ((res.measured_left, got.measured_left),
+                             (res.measured_right, got.measured_right),
+                             (res.fused.left, got.fused.left), (res.fused.right, got.fused.right)):
+                    assert np.array_equal(a.values, b.values) and np.array_equal(a.valid, b.valid)
+                assert np.array_equal(res.intervals_left.lo, got.intervals_left.lo)
+                assert res.search_fraction_left == got.search_fraction_left
+        assert got.search_fraction_left < 1.0
+    finally:
+        bench.use_config(5)

@@ -542,7 +542,7 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   // measured: the 4-lane kernel wins up to ~60% search fraction
   static const double split = getenv("ES_SGM_SPLIT") ? atof(getenv("ES_SGM_SPLIT")) : 0.6;
   sa.split = split;
-  if (c->arith == ARITH_U16 && !c->lanes && getenv("ES_SGM_VAR") == nullptr) {
+  if (c->arith == ARITH_U16 && !c->lanes) {
     // fork: the partial sums' families and the two regime variants run on
     // 2 * parts concurrent streams; each touches its own (seq, view) x sum
     const int P = c->parts;

@@ -106,131 +106,6 @@ __global__ void __launch_bounds__(COST_NT) k_cost(CostArgs a) {
   }
 }
 
-// Runs of COST_R consecutive pairs per thread: one binary search per run,
-// pixel state carried across pairs, and for window 3 a clamp-free fast path
-// (interior match columns) where the pair's two cells share four columns of
-// the other image: 4 LDS + 6 VABSDIFF4 per pair.
-constexpr int COST_R = 4;
-
-__global__ void __launch_bounds__(COST_NT) k_cost_w3(CostArgs a) {
-  extern __shared__ uint32_t sm[];
-  const int W = a.W, H = a.H;
-  const int y = blockIdx.x;
-  const int svl = blockIdx.y;
-  const int svg = a.view0 + svl;
-  const int view = svg & 1, seq = svg >> 1;
-  uint32_t* refcol = sm;            // [W]
-  uint32_t* othcol = sm + W;        // [W]
-  uint32_t* rowoff = sm + 2 * W;    // [W + 1]
-  uint32_t* rowlh = sm + 3 * W + 1; // [W]
-  const size_t HW = (size_t)W * H;
-  const uint8_t* ref = a.img + ((size_t)seq * 2 + view) * HW;
-  const uint8_t* oth = a.img + ((size_t)seq * 2 + (view ^ 1)) * HW;
-  const uint2* meta = a.meta + (size_t)svl * HW + (size_t)y * W;
-  const uint32_t rowbase = (uint32_t)(y * row_capacity(W, a.d_max));
-  const int y0 = max(y - 1, 0), y2 = min(y + 1, H - 1);
-  for (int x = threadIdx.x; x < W; x += COST_NT) {
-    refcol[x] = (uint32_t)ref[(size_t)y0 * W + x] | ((uint32_t)ref[(size_t)y * W + x] << 8) |
-                ((uint32_t)ref[(size_t)y2 * W + x] << 16);
-    othcol[x] = (uint32_t)oth[(size_t)y0 * W + x] | ((uint32_t)oth[(size_t)y * W + x] << 8) |
-                ((uint32_t)oth[(size_t)y2 * W + x] << 16);
-    const uint2 m = meta[x];
-    rowoff[x] = m.y - rowbase;
-    rowlh[x] = m.x;
-  }
-  __syncthreads();
-  // the row's slots up to the end of the last pixel's allocation (its
-  // trailing padding slot included: padding holds +inf)
-  const uint32_t last = rowlh[W - 1];
-  const uint32_t row_pairs = rowoff[W - 1] - pad_before(last & 0xFFFFu) +
-                             pixel_slots(last & 0xFFFFu, last >> 16);
-  if (threadIdx.x == 0) rowoff[W] = row_pairs;
-  __syncthreads();
-  const uint32_t border = 9u * 255u;
-  uint32_t* C = a.C + (size_t)svl * a.volcap + rowbase;
-  const int sign = view == 0 ? -1 : 1;
-  for (uint32_t q0 = threadIdx.x * COST_R; q0 < row_pairs; q0 += COST_NT * COST_R) {
-    int lo_i = 0, hi_i = W - 1;
-    while (lo_i < hi_i) {
-      const int mid = (lo_i + hi_i + 1) >> 1;
-      if (rowoff[mid] <= q0) lo_i = mid; else hi_i = mid - 1;
-    }
-    int x = lo_i;
-    uint32_t beg = rowoff[x], end = rowoff[x + 1];
-    uint32_t lh = rowlh[x];
-    uint32_t r0 = refcol[max(x - 1, 0)], r1 = refcol[x], r2 = refcol[min(x + 1, W - 1)];
-    uint32_t out[COST_R];
-#pragma unroll
-    for (int r = 0; r < COST_R; ++r) {
-      const uint32_t q = q0 + r;
-      out[r] = INF16x2;
-      if (q >= row_pairs) continue;
-      if (q >= end) {   // next pixel (every pixel owns >= 1 pair)
-        ++x;
-        beg = end;
-        end = rowoff[x + 1];
-        lh = rowlh[x];
-        r0 = refcol[max(x - 1, 0)];
-        r1 = refcol[x];
-        r2 = refcol[min(x + 1, W - 1)];
-      }
-      const int lo = lh & 0xFFFF, hi = lh >> 16;
-      const int d0 = 2 * ((lo >> 1) + (int)(q - beg));
-      // match columns of the two cells: x + ox + sign*d, ox in {-1,0,1},
-      // d in {d0, d0+1}; interior when all four lie inside the image
-      const int cmin = sign < 0 ? x - 1 - (d0 + 1) : x - 1 + d0;
-      const int cmax = sign < 0 ? x + 1 - d0 : x + 1 + d0 + 1;
-      uint32_t c0, c1;
-      if (x >= 1 && x <= W - 2 && cmin >= 0 && cmax <= W - 1) {
-        // left view: cell d uses columns x-1-d .. x+1-d; cell d+1 one to the left
-        const int b = sign < 0 ? x - 2 - d0 : x - 1 + d0;   // lowest of the 4 columns
-        const uint32_t o0 = othcol[b], o1 = othcol[b + 1], o2 = othcol[b + 2], o3 = othcol[b + 3];
-        if (sign < 0) {
-          c0 = __vsadu4(r0, o1) + __vsadu4(r1, o2) + __vsadu4(r2, o3);
-          c1 = __vsadu4(r0, o0) + __vsadu4(r1, o1) + __vsadu4(r2, o2);
-        } else {
-          c0 = __vsadu4(r0, o0) + __vsadu4(r1, o1) + __vsadu4(r2, o2);
-          c1 = __vsadu4(r0, o1) + __vsadu4(r1, o2) + __vsadu4(r2, o3);
-        }
-      } else {
-        uint32_t cc[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int d = d0 + h;
-          const int xm = x + sign * d;
-          if (xm < 0 || xm > W - 1) {
-            cc[h] = border;
-          } else {
-            uint32_t sad = 0;
-#pragma unroll
-            for (int ox = -1; ox <= 1; ++ox) {
-              const int xx = clampi(x + ox, 0, W - 1);
-              sad = __vsadu4(refcol[xx], othcol[clampi(xx + sign * d, 0, W - 1)]) + sad;
-            }
-            cc[h] = sad;
-          }
-        }
-        c0 = cc[0];
-        c1 = cc[1];
-      }
-      // off-image centres take the border cost; cells outside [lo, hi] are +inf
-      if ((unsigned)(x + sign * d0) > (unsigned)(W - 1)) c0 = border;
-      if ((unsigned)(x + sign * (d0 + 1)) > (unsigned)(W - 1)) c1 = border;
-      // (padding slots lie wholly outside [lo, hi])
-      if (d0 < lo || d0 > hi) c0 = INF16;
-      if (d0 + 1 < lo || d0 + 1 > hi) c1 = INF16;
-      out[r] = c0 | (c1 << 16);
-    }
-    if (q0 + COST_R <= row_pairs && ((rowbase + q0) & 3u) == 0 && ((a.volcap * svl) & 3u) == 0) {
-      *reinterpret_cast<uint4*>(C + q0) = make_uint4(out[0], out[1], out[2], out[3]);
-    } else {
-#pragma unroll
-      for (int r = 0; r < COST_R; ++r)
-        if (q0 + r < row_pairs) C[q0 + r] = out[r];
-    }
-  }
-}
-
 // Window 3, run-table schedule.  Every pixel's allocation is a whole number
 // of aligned 4-pair runs (8 cells, one 16-byte word; es_common.cuh), and a
 // row's allocations are consecutive, so a warp that owns 32 consecutive
@@ -371,21 +246,13 @@ __device__ __forceinline__ void cost_runs_row(const CostArgs& a, int rmax) {
 }
 
 void launch_cost(const CostArgs& a, int n_sv, cudaStream_t st) {
-  static const bool runs = getenv("ES_COST_W3") == nullptr;   // A/B switch
-  if (a.window == 3 && runs) {
+  if (a.window == 3) {
     const int rmax = (npairs_max(a.d_max) + 3) / 4;   // runs per pixel, at most
     dim3 grid(a.H, n_sv);
     const size_t smem = sizeof(uint32_t) * (2 * (size_t)a.W + 2 * (size_t)cost_pad_cols(a.d_max)) +
                         (size_t)CR_WARPS * 32 * rmax;
     cudaFuncSetAttribute(k_cost_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_cost_runs<<<grid, CR_WARPS * 32, smem, st>>>(a, rmax);
-    return;
-  }
-  if (a.window == 3 && getenv("ES_COST_V1") == nullptr) {
-    dim3 grid(a.H, n_sv);
-    const size_t smem = sizeof(uint32_t) * (4 * (size_t)a.W + 1);
-    cudaFuncSetAttribute(k_cost_w3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_cost_w3<<<grid, COST_NT, smem, st>>>(a);
     return;
   }
   const int nw = (a.window + 3) / 4;

@@ -257,162 +257,7 @@ __device__ __forceinline__ bool grp_pixel(int fam, int bwd, int c, int t, int W,
   return x >= 0 && x < W && c < W + H - 1;
 }
 
-template <int G, int NCH>
-__global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp(SgmArgs a, int fam, int sweeps,
-                                                             int init) {
-  constexpr int NG = 32 / G;
-  constexpr uint32_t NONE = 0xFFFFFFFFu;
-  const int lane = threadIdx.x & 31;
-  const int gl = lane & (G - 1);
-  const int grp = lane / G;
-  const int gbase = lane & ~(G - 1);
-  const int W = a.W, H = a.H;
-  const int nchains = fam == FAM_H ? H : (fam == FAM_V ? W : W + H - 1);
-  const int c0 = (blockIdx.x * GRP_WARPS + (threadIdx.x >> 5)) * NG;
-  if (c0 >= nchains) return;
-  if (a.select) {   // per-(seq, view) choice of G from the frame's searched cells
-    const double frac = (double)a.cells[blockIdx.y] / ((double)W * H * (a.d_max + 1));
-    if ((a.select == 1) == (frac > a.split)) return;
-  }
-  const int ch = c0 + grp;
-  const size_t HW = (size_t)W * H;
-  const uint2* __restrict__ meta = a.meta + (size_t)blockIdx.y * HW;
-  const uint32_t* __restrict__ C =
-      reinterpret_cast<const uint32_t*>(a.C) + (size_t)blockIdx.y * a.volcap;
-  uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
-  // keep the per-(seq, view) bases in registers (ptxas otherwise re-derives
-  // them from the parameter bank at every load and store)
-#ifndef ES_GRP3_NOPIN
-  asm volatile("" : "+l"(C));
-  asm volatile("" : "+l"(S));
-#endif
-  const uint32_t p1x2 = a.p1i * 0x10001u;
-  const uint32_t p2 = a.p2i;
-  const int len = fam == FAM_H ? W : H;
-  const int src_l = gbase | ((gl + G - 1) & (G - 1));
-  const int src_r = gbase | ((gl + 1) & (G - 1));
-  bool first_sweep = true;
-  for (int bwd = 0; bwd < 2; ++bwd) {
-    if (!(sweeps & (1 << bwd))) continue;
-    const bool init_sum = init && first_sweep;
-    first_sweep = false;
-    // meta batches: lane g of a group holds the meta of step tb + g
-    auto load_meta = [&](int tb) -> uint2 {
-      int x, y;
-      const int t = tb + gl;
-      if (t < len && grp_pixel(fam, bwd, ch, t, W, H, x, y)) return meta[(size_t)y * W + x];
-      return make_uint2(NONE, 0u);   // no pixel on this step
-    };
-    uint2 mb_cur = load_meta(0);
-    uint2 mb_next = load_meta(G);
-    int tb = 0;
-    // chunk c of this group: pairs c*G + gl; a step's operands are valid for
-    // rel = c*G + gl - j0 < span (span = 0 when the chain has no pixel)
-    auto umask = [](int lo, int hi) -> uint32_t {   // chunks lo..hi as a bit mask
-      return hi < lo ? 0u : ((hi >= 31 ? 0xFFFFFFFFu : ((2u << hi) - 1u)) & ~((1u << lo) - 1u));
-    };
-    uint32_t prev[NCH], cn[NCH], sn[NCH];
-    // step 0's meta, chunk range and prefetched operands
-    const uint32_t mx0 = __shfl_sync(FULL, mb_cur.x, gbase);
-    uint32_t my = __shfl_sync(FULL, mb_cur.y, gbase);
-    bool act = mx0 != NONE;
-    int j0 = (int)((mx0 & 0xFFFFu) >> 1);
-    uint32_t span = act ? (uint32_t)((int)((mx0 >> 16) >> 1) - j0 + 1) : 0u;
-    uint32_t um = umask(__reduce_min_sync(FULL, act ? j0 / G : NCH),
-                        __reduce_max_sync(FULL, act ? (int)((mx0 >> 16) >> 1) / G : -1));
-#pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-      prev[c] = INF16x2;
-      const uint32_t rel = (uint32_t)(c * G + gl - j0);
-      const bool in = ((um >> c) & 1u) && rel < span;
-      cn[c] = in ? __ldg(C + (my + rel)) : INF16x2;
-      sn[c] = (in && !init_sum) ? S[my + rel] : 0u;
-    }
-    uint32_t m = 0;
-    bool was_active = false;
-    for (int t = 0; t < len; ++t) {
-      // ---- the next step's meta and chunk mask (prefetch target)
-      int j0n = 0;
-      uint32_t my1 = 0, span1 = 0;
-      int clo1 = NCH, chi1 = -1;
-      if (t + 1 < len) {
-        if (t + 1 == tb + G) {   // step t+1 opens the next batch: rotate, and
-          tb += G;               // issue the batch after it (used G steps later)
-          mb_cur = mb_next;
-          mb_next = load_meta(tb + G);
-        }
-        const int r = t + 1 - tb;   // 0 .. G-1
-        const uint32_t mx1 = __shfl_sync(FULL, mb_cur.x, gbase | r);
-        my1 = __shfl_sync(FULL, mb_cur.y, gbase | r);
-        if (mx1 != NONE) {
-          j0n = (int)((mx1 & 0xFFFFu) >> 1);
-          const int j1n = (int)((mx1 >> 16) >> 1);
-          span1 = (uint32_t)(j1n - j0n + 1);
-          clo1 = j0n / G;
-          chi1 = j1n / G;
-        }
-      }
-      const uint32_t um1 = umask(__reduce_min_sync(FULL, clo1), __reduce_max_sync(FULL, chi1));
-      // ---- this step
-      const bool first = act && !was_active;
-      const uint32_t mp2 = (m + p2) * 0x10001u;
-      const uint32_t ng = ((0x10000u - m) & 0xFFFFu) * 0x10001u;
-      uint32_t nmin = INF16x2;
-      uint32_t left_old = INF16x2;   // prev[c-1] before this step overwrote it
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        const uint32_t pv = prev[c];
-        if ((um >> c) & 1u) {
-          const uint32_t srcl = gl == G - 1 ? left_old : pv;
-          const uint32_t srcr = gl == 0 ? (c + 1 < NCH ? prev[c + 1 < NCH ? c + 1 : c] : INF16x2) : pv;
-          const uint32_t pl = __shfl_sync(FULL, srcl, src_l);
-          const uint32_t pr = __shfl_sync(FULL, srcr, src_r);
-          const uint32_t nb = __vminu2(__byte_perm(pl, pv, 0x5432), __byte_perm(pv, pr, 0x5432));
-          const uint32_t cand = __vminu2(__viaddmin_u16x2(nb, p1x2, pv), mp2);
-          // chunks outside this chain's own range carry cn = +inf, so L lands
-          // in the [0x8000, 0x8000 + P2] band and is never selected
-          const uint32_t L = first ? cn[c] : __vadd2(cn[c], __vadd2(cand, ng));
-          prev[c] = L;
-          nmin = __vminu2(nmin, L);
-          const uint32_t rel = (uint32_t)(c * G + gl - j0);
-          if (rel < span) S[my + rel] = init_sum ? L : __vadd2(sn[c], L);
-        } else {
-          prev[c] = INF16x2;
-        }
-        left_old = pv;
-        // refill chunk c for step t+1 (after its use above)
-        if ((um1 >> c) & 1u) {
-          const uint32_t rel = (uint32_t)(c * G + gl - j0n);
-          const bool in = rel < span1;
-          cn[c] = in ? __ldg(C + (my1 + rel)) : INF16x2;
-          sn[c] = (in && !init_sum) ? S[my1 + rel] : 0u;
-        }
-      }
-      // per-chain minimum: one REDUX per group over masked values
-      const uint32_t hm = min(nmin & 0xFFFFu, nmin >> 16);
-      uint32_t mg = 0;
-#pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        const uint32_t r = __reduce_min_sync(FULL, grp == g ? hm : 0xFFFFFFFFu);
-        if (grp == g) mg = r;
-      }
-      m = mg;
-      was_active = act;
-      act = span1 != 0;
-      j0 = j0n;
-      my = my1;
-      span = span1;
-      um = um1;
-    }
-  }
-}
-
-// ------------------------------------------------------------ grouped, depth 2
-//
-// k_sgm_grp with the operands fetched two steps ahead: two register sets
-// alternate (the step loop is unrolled by two so both stay statically
-// indexed), giving each load about two steps of compute to land.
-
+// per-step scalars of one chain for k_sgm_grp3
 struct GrpStep {          // per-step scalars of one chain (uniform in its group)
   uint32_t my;            // pair offset of the pixel
   int j0;                 // first pair
@@ -420,179 +265,12 @@ struct GrpStep {          // per-step scalars of one chain (uniform in its group
   uint32_t um;            // warp-uniform chunk mask (union over the warp's chains)
 };
 
-template <int G, int NCH, int PF>
-__global__ void __launch_bounds__(GRP_WARPS * 32) k_sgm_grp2(SgmArgs a, int fam, int sweeps,
-                                                              int init) {
-  constexpr int NG = 32 / G;
-  constexpr uint32_t NONE = 0xFFFFFFFFu;
-  const int lane = threadIdx.x & 31;
-  const int gl = lane & (G - 1);
-  const int grp = lane / G;
-  const int gbase = lane & ~(G - 1);
-  const int W = a.W, H = a.H;
-  const int nchains = fam == FAM_H ? H : (fam == FAM_V ? W : W + H - 1);
-  const int c0 = (blockIdx.x * GRP_WARPS + (threadIdx.x >> 5)) * NG;
-  if (c0 >= nchains) return;
-  if (a.select) {
-    const double frac = (double)a.cells[blockIdx.y] / ((double)W * H * (a.d_max + 1));
-    if ((a.select == 1) == (frac > a.split)) return;
-  }
-  const int ch = c0 + grp;
-  const size_t HW = (size_t)W * H;
-  const uint2* __restrict__ meta = a.meta + (size_t)blockIdx.y * HW;
-  const uint32_t* __restrict__ C =
-      reinterpret_cast<const uint32_t*>(a.C) + (size_t)blockIdx.y * a.volcap;
-  uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
-#ifndef ES_GRP3_NOPIN
-  asm volatile("" : "+l"(C));
-  asm volatile("" : "+l"(S));
-#endif
-  const uint32_t p1x2 = a.p1i * 0x10001u;
-  const uint32_t p2 = a.p2i;
-  const int len = fam == FAM_H ? W : H;
-  const int src_l = gbase | ((gl + G - 1) & (G - 1));
-  const int src_r = gbase | ((gl + 1) & (G - 1));
-  auto umask = [](int lo, int hi) -> uint32_t {
-    return hi < lo ? 0u : ((hi >= 31 ? 0xFFFFFFFFu : ((2u << hi) - 1u)) & ~((1u << lo) - 1u));
-  };
-  bool first_sweep = true;
-  for (int bwd = 0; bwd < 2; ++bwd) {
-    if (!(sweeps & (1 << bwd))) continue;
-    const bool init_sum = init && first_sweep;
-    first_sweep = false;
-    auto load_meta = [&](int tb) -> uint2 {
-      int x, y;
-      const int t = tb + gl;
-      if (t < len && grp_pixel(fam, bwd, ch, t, W, H, x, y)) return meta[(size_t)y * W + x];
-      return make_uint2(NONE, 0u);
-    };
-    uint2 mb_cur = load_meta(0);
-    uint2 mb_next = load_meta(G);
-    int tb = 0;
-    // scalars of step t' (t' < len), from the two meta batches
-    auto info = [&](int tp) -> GrpStep {
-      GrpStep s{0u, 0, 0u, 0u};
-      int clo = NCH, chi = -1;
-      if (tp < len) {
-        if (tp == tb + G) {   // rotate the batches; the new one is used G steps later
-          tb += G;
-          mb_cur = mb_next;
-          mb_next = load_meta(tb + G);
-        }
-        const int r = tp - tb;
-        const uint32_t mx = __shfl_sync(FULL, mb_cur.x, gbase | r);
-        s.my = __shfl_sync(FULL, mb_cur.y, gbase | r);
-        if (mx != NONE) {
-          s.j0 = (int)((mx & 0xFFFFu) >> 1);
-          const int j1 = (int)((mx >> 16) >> 1);
-          s.span = (uint32_t)(j1 - s.j0 + 1);
-          clo = s.j0 / G;
-          chi = j1 / G;
-        }
-      }
-      s.um = umask(__reduce_min_sync(FULL, clo), __reduce_max_sync(FULL, chi));
-      return s;
-    };
-    auto fetch = [&](const GrpStep& s, uint32_t (&cn)[NCH], uint32_t (&sn)[NCH], int c) {
-      const uint32_t rel = (uint32_t)(c * G + gl - s.j0);
-      const bool in = rel < s.span;
-      cn[c] = in ? __ldg(C + (s.my + rel)) : INF16x2;
-      sn[c] = (in && !init_sum) ? S[s.my + rel] : 0u;
-    };
-    uint32_t prev[NCH], cs[PF][NCH], ss[PF][NCH];
-    GrpStep sq[PF];
-#pragma unroll
-    for (int p = 0; p < PF; ++p) sq[p] = info(p);
-#pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-      prev[c] = INF16x2;
-#pragma unroll
-      for (int p = 0; p < PF; ++p) fetch(sq[p], cs[p], ss[p], c);
-    }
-    uint32_t m = 0;
-    bool was_active = false;
-    // one step: consume (cn, sn) for step t (scalars cur), refill them with
-    // step t+2 (scalars nn)
-    auto step = [&](const GrpStep& cur, const GrpStep& nn, uint32_t (&cn)[NCH],
-                    uint32_t (&sn)[NCH]) {
-      const bool act = cur.span != 0;
-      const bool first = act && !was_active;
-      const uint32_t mp2 = (m + p2) * 0x10001u;
-      const uint32_t ng = ((0x10000u - m) & 0xFFFFu) * 0x10001u;
-      uint32_t nmin = INF16x2;
-      uint32_t left_old = INF16x2;
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        const uint32_t pv = prev[c];
-        if ((cur.um >> c) & 1u) {
-          const uint32_t srcl = gl == G - 1 ? left_old : pv;
-          const uint32_t srcr =
-              gl == 0 ? (c + 1 < NCH ? prev[c + 1 < NCH ? c + 1 : c] : INF16x2) : pv;
-          const uint32_t pl = __shfl_sync(FULL, srcl, src_l);
-          const uint32_t pr = __shfl_sync(FULL, srcr, src_r);
-          const uint32_t nb = __vminu2(__byte_perm(pl, pv, 0x5432), __byte_perm(pv, pr, 0x5432));
-          const uint32_t cand = __vminu2(__viaddmin_u16x2(nb, p1x2, pv), mp2);
-          const uint32_t L = first ? cn[c] : __vadd2(cn[c], __vadd2(cand, ng));
-          prev[c] = L;
-          nmin = __vminu2(nmin, L);
-          const uint32_t rel = (uint32_t)(c * G + gl - cur.j0);
-          if (rel < cur.span) S[cur.my + rel] = init_sum ? L : __vadd2(sn[c], L);
-        } else {
-          prev[c] = INF16x2;
-        }
-        left_old = pv;
-        if ((nn.um >> c) & 1u) fetch(nn, cn, sn, c);
-      }
-      const uint32_t hm = min(nmin & 0xFFFFu, nmin >> 16);
-      uint32_t mg = 0;
-#pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        const uint32_t r = __reduce_min_sync(FULL, grp == g ? hm : 0xFFFFFFFFu);
-        if (grp == g) mg = r;
-      }
-      m = mg;
-      was_active = act;
-    };
-    for (int t = 0; t < len; t += PF) {
-#pragma unroll
-      for (int p = 0; p < PF; ++p) {
-        if (t + p < len) {
-          const GrpStep nx = info(t + p + PF);
-          step(sq[p], nx, cs[p], ss[p]);
-          sq[p] = nx;
-        }
-      }
-    }
-  }
-}
-
-template <int G>
-static void launch_grp2(const SgmArgs& a, int nch_pairs, int fam, int sweeps, int init, int n_sv,
-                        cudaStream_t st) {
-  const int nchains = fam == FAM_H ? a.H : (fam == FAM_V ? a.W : a.W + a.H - 1);
-  constexpr int per_block = GRP_WARPS * (32 / G);
-  dim3 grid((nchains + per_block - 1) / per_block, n_sv);
-  const int nch = (nch_pairs + G - 1) / G;
-  static const int pf = getenv("ES_SGM_PF") ? atoi(getenv("ES_SGM_PF")) : 3;
-  auto go = [&](auto kern) { kern<<<grid, GRP_WARPS * 32, 0, st>>>(a, fam, sweeps, init); };
-  if (nch <= 4) {
-    if (pf <= 2) go(k_sgm_grp2<G, 4, 2>);
-    else if (pf == 3) go(k_sgm_grp2<G, 4, 3>);
-    else go(k_sgm_grp2<G, 4, 4>);
-  } else if (nch <= 8) {
-    if (pf <= 2) go(k_sgm_grp2<G, 8, 2>);
-    else if (pf == 3) go(k_sgm_grp2<G, 8, 3>);
-    else go(k_sgm_grp2<G, 8, 4>);
-  } else if (nch <= 16) {
-    go(k_sgm_grp2<G, 16, 2>);
-  } else {
-    go(k_sgm_grp2<G, 32, 2>);
-  }
-}
-
 // ------------------------------------------------------------ grouped, 2 pairs/lane
 //
-// As k_sgm_grp2 (two-step-ahead operand prefetch) but every lane owns two
+// The round's previous production kernel, kept as the A/B baseline of
+// k_sgm_grp4 (ES_SGM_G4=0): operands fetched two steps ahead into two
+// alternating register sets, metadata batches broadcast by shuffle, and every
+// lane owns two
 // consecutive pairs (4 cells): lane g of chunk c holds pairs
 // c*2G + 2g and c*2G + 2g + 1.  The shuffles, selects, chunk-mask tests and
 // address arithmetic are shared by four cells, and the byte permute that
@@ -1107,260 +785,6 @@ static void launch_grp4(const SgmArgs& a, int fam, int init, int n_sv, cudaStrea
   else go(k_sgm_grp4<G, 8, PPL, MINB>);
 }
 
-// ------------------------------------------------------------ v4 (u16)
-//
-// Same lane mapping as k_sgm_grp, but the predecessor's path values live in
-// shared memory (absolute pair index, double-buffered), so a step loops
-// dynamically over just the union of its chains' chunks, and the next
-// step's cost / partial-sum pairs are staged into shared memory with
-// cp.async while the current step computes.
-
-constexpr int V4_WARPS = 8;
-
-__device__ __forceinline__ void cp_async4(uint32_t* smem_dst, const uint32_t* gsrc) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait1() {
-  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-}
-
-template <int G>
-__global__ void __launch_bounds__(V4_WARPS * 32) k_sgm_v4(SgmArgs a, int fam, int sweeps,
-                                                           int init) {
-  constexpr int NG = 32 / G;
-  constexpr uint32_t NONE = 0xFFFFFFFFu;
-  extern __shared__ uint32_t v4smem[];
-  const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
-  const int gl = lane & (G - 1);
-  const int grp = lane / G;
-  const int gbase = lane & ~(G - 1);
-  const int W = a.W, H = a.H;
-  const int NP = npairs_max(a.d_max);
-  const int NPP = NP + 2;
-  const int nchains = fam == FAM_H ? H : (fam == FAM_V ? W : W + H - 1);
-  const int c0 = (blockIdx.x * V4_WARPS + wid) * NG;
-  if (c0 >= nchains) return;
-  if (a.select) {
-    const double frac = (double)a.cells[blockIdx.y] / ((double)W * H * (a.d_max + 1));
-    if ((a.select == 1) == (frac > a.split)) return;
-  }
-  // per-warp shared memory: pbuf[2][NG][NPP], cst[2][NG][NP], sst[2][NG][NP]
-  uint32_t* wsm = v4smem + (size_t)wid * (2 * NG * NPP + 4 * NG * NP);
-  uint32_t* pbuf = wsm;
-  uint32_t* cst = wsm + 2 * NG * NPP;
-  uint32_t* sst = cst + 2 * NG * NP;
-  const int ch = c0 + grp;
-  const size_t HW = (size_t)W * H;
-  const uint2* __restrict__ meta = a.meta + (size_t)blockIdx.y * HW;
-  const uint32_t* __restrict__ C =
-      reinterpret_cast<const uint32_t*>(a.C) + (size_t)blockIdx.y * a.volcap;
-  uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
-  asm volatile("" : "+l"(C));
-  asm volatile("" : "+l"(S));
-  const uint32_t p1x2 = a.p1i * 0x10001u;
-  const uint32_t p2 = a.p2i;
-  const int len = fam == FAM_H ? W : H;
-  bool first_sweep = true;
-  for (int bwd = 0; bwd < 2; ++bwd) {
-    if (!(sweeps & (1 << bwd))) continue;
-    const bool init_sum = init && first_sweep;
-    first_sweep = false;
-    auto load_meta = [&](int tb) -> uint2 {
-      int x, y;
-      const int t = tb + gl;
-      if (t < len && grp_pixel(fam, bwd, ch, t, W, H, x, y)) return meta[(size_t)y * W + x];
-      return make_uint2(NONE, 0u);
-    };
-    // stage the operands of one step: group lanes copy its pairs
-    auto stage = [&](int slot, uint32_t my_, int span_) {
-      uint32_t* cd = cst + (slot * NG + grp) * NP;
-      uint32_t* sd = sst + (slot * NG + grp) * NP;
-      const int rounds = __reduce_max_sync(FULL, (span_ + G - 1) / G);
-      for (int k = 0; k < rounds; ++k) {
-        const int i = k * G + gl;
-        if (i < span_) {
-          cp_async4(cd + i, C + (my_ + (uint32_t)i));
-          if (!init_sum) cp_async4(sd + i, S + (my_ + (uint32_t)i));
-        }
-      }
-      cp_async_commit();
-    };
-    uint2 mb_cur = load_meta(0);
-    uint2 mb_next = load_meta(G);
-    int tb = 0;
-    const uint32_t mx0 = __shfl_sync(FULL, mb_cur.x, gbase);
-    uint32_t my = __shfl_sync(FULL, mb_cur.y, gbase);
-    int j0 = 0, j1 = -1;
-    if (mx0 != NONE) {
-      j0 = (int)((mx0 & 0xFFFFu) >> 1);
-      j1 = (int)((mx0 >> 16) >> 1);
-    }
-    int jp0 = 0, jp1 = -1;   // predecessor's pair range (empty: no predecessor)
-    stage(0, my, j1 - j0 + 1);
-    uint32_t m = 0;
-    int rp = 0;
-    for (int t = 0; t < len; ++t) {
-      // ---- next step: meta, stage its operands
-      int j0n = 0, j1n = -1;
-      uint32_t my1 = 0;
-      if (t + 1 < len) {
-        if (t + 1 == tb + G) {
-          tb += G;
-          mb_cur = mb_next;
-          mb_next = load_meta(tb + G);
-        }
-        const int r = t + 1 - tb;
-        const uint32_t mx1 = __shfl_sync(FULL, mb_cur.x, gbase | r);
-        my1 = __shfl_sync(FULL, mb_cur.y, gbase | r);
-        if (mx1 != NONE) {
-          j0n = (int)((mx1 & 0xFFFFu) >> 1);
-          j1n = (int)((mx1 >> 16) >> 1);
-        }
-      }
-      stage((t + 1) & 1, my1, j1n - j0n + 1);
-      cp_async_wait1();   // this step's staged operands have landed
-      __syncwarp();
-      // ---- this step over the union of the chains' chunks
-      const bool act = j1 >= j0;
-      const bool first = act && jp1 < jp0;
-      const int ulo = __reduce_min_sync(FULL, act ? j0 / G : 0x7fff);
-      const int uhi = __reduce_max_sync(FULL, act ? j1 / G : -1);
-      const uint32_t mp2 = (m + p2) * 0x10001u;
-      const uint32_t ng = ((0x10000u - m) & 0xFFFFu) * 0x10001u;
-      const uint32_t* pr_ = pbuf + (rp * NG + grp) * NPP + 1;        // predecessor
-      uint32_t* pw_ = pbuf + ((rp ^ 1) * NG + grp) * NPP + 1;        // this pixel
-      const uint32_t* cs = cst + ((t & 1) * NG + grp) * NP;
-      const uint32_t* ss = sst + ((t & 1) * NG + grp) * NP;
-      const uint32_t pspan = (uint32_t)(jp1 - jp0 + 1);
-      const uint32_t span = (uint32_t)(j1 - j0 + 1);
-      uint32_t nmin = INF16x2;
-      for (int c = ulo; c <= uhi; ++c) {
-        const int j = c * G + gl;
-        const uint32_t rel = (uint32_t)(j - j0);
-        const bool in = rel < span;
-        if (in) {
-          const uint32_t cv = cs[rel];
-          uint32_t L;
-          if (first) {
-            L = cv;
-          } else {
-            const uint32_t pv = (uint32_t)(j - jp0) < pspan ? pr_[j] : INF16x2;
-            const uint32_t pl = (uint32_t)(j - 1 - jp0) < pspan ? pr_[j - 1] : INF16x2;
-            const uint32_t pr = (uint32_t)(j + 1 - jp0) < pspan ? pr_[j + 1] : INF16x2;
-            const uint32_t nb =
-                __vminu2(__byte_perm(pl, pv, 0x5432), __byte_perm(pv, pr, 0x5432));
-            const uint32_t cand = __vminu2(__viaddmin_u16x2(nb, p1x2, pv), mp2);
-            L = __vadd2(cv, __vadd2(cand, ng));
-          }
-          pw_[j] = L;
-          nmin = __vminu2(nmin, L);
-          S[my + rel] = init_sum ? L : __vadd2(ss[rel], L);
-        }
-      }
-      const uint32_t hm = min(nmin & 0xFFFFu, nmin >> 16);
-      uint32_t mg = 0;
-#pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        const uint32_t r = __reduce_min_sync(FULL, grp == g ? hm : 0xFFFFFFFFu);
-        if (grp == g) mg = r;
-      }
-      __syncwarp();   // this step's pbuf writes / stage reads before reuse
-      m = mg;
-      jp0 = j0;
-      jp1 = j1;
-      j0 = j0n;
-      j1 = j1n;
-      my = my1;
-      rp ^= 1;
-    }
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncwarp();
-  }
-}
-
-template <int G>
-static void launch_v4(const SgmArgs& a, int fam, int sweeps, int init, int n_sv, cudaStream_t st) {
-  const int nchains = fam == FAM_H ? a.H : (fam == FAM_V ? a.W : a.W + a.H - 1);
-  constexpr int NG = 32 / G;
-  constexpr int per_block = V4_WARPS * NG;
-  const int NP = npairs_max(a.d_max);
-  const size_t smem = sizeof(uint32_t) * V4_WARPS * (2 * NG * (NP + 2) + 4 * NG * NP);
-  dim3 grid((nchains + per_block - 1) / per_block, n_sv);
-  cudaFuncSetAttribute(k_sgm_v4<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_sgm_v4<G><<<grid, V4_WARPS * 32, smem, st>>>(a, fam, sweeps, init);
-}
-
-template <int G>
-static void launch_grp(const SgmArgs& a, int nch_pairs, int fam, int sweeps, int init, int n_sv,
-                       cudaStream_t st) {
-  const int nchains = fam == FAM_H ? a.H : (fam == FAM_V ? a.W : a.W + a.H - 1);
-  constexpr int per_block = GRP_WARPS * (32 / G);
-  dim3 grid((nchains + per_block - 1) / per_block, n_sv);
-  const int nch = (nch_pairs + G - 1) / G;
-  if (nch <= 2) k_sgm_grp<G, 2><<<grid, GRP_WARPS * 32, 0, st>>>(a, fam, sweeps, init);
-  else if (nch <= 4) k_sgm_grp<G, 4><<<grid, GRP_WARPS * 32, 0, st>>>(a, fam, sweeps, init);
-  else if (nch <= 8) k_sgm_grp<G, 8><<<grid, GRP_WARPS * 32, 0, st>>>(a, fam, sweeps, init);
-  else if (nch <= 16) k_sgm_grp<G, 16><<<grid, GRP_WARPS * 32, 0, st>>>(a, fam, sweeps, init);
-  else k_sgm_grp<G, 32><<<grid, GRP_WARPS * 32, 0, st>>>(a, fam, sweeps, init);
-}
-
-static void launch_family_seg(const SgmArgs& a, int fam, int sweeps, int init, int n_sv,
-                              cudaStream_t st) {
-  static const int forced = getenv("ES_SGM_G") ? atoi(getenv("ES_SGM_G")) : 0;
-  static const bool use_v3 = getenv("ES_SGM_V3") != nullptr;   // A/B switch
-  const int np = npairs_max(a.d_max);
-  if (!use_v3) {
-    if (!forced && !a.lanes && a.cells) {
-      // measured: reduced intervals run best in the shared-memory
-      // v4 kernel with 8 lanes per chain, wide ones in the register kernel
-      // with 16 lanes per chain
-      SgmArgs lo = a, hi = a;
-      lo.select = 1;
-      hi.select = 2;
-      static const int variant = getenv("ES_SGM_VAR") ? atoi(getenv("ES_SGM_VAR")) : 0;
-      if (variant == 1) {          // one pair per lane, depth-2 prefetch
-        launch_grp2<8>(lo, np, fam, sweeps, init, n_sv, st);
-        launch_grp2<16>(hi, np, fam, sweeps, init, n_sv, st);
-      } else if (variant == 2) {   // shared-memory v4 for reduced intervals
-        launch_v4<8>(lo, fam, sweeps, init, n_sv, st);
-        launch_grp2<16>(hi, np, fam, sweeps, init, n_sv, st);
-      } else if (variant == 3) {   // two pairs per lane, 16 lanes for wide intervals
-        launch_v4<8>(lo, fam, sweeps, init, n_sv, st);
-        launch_grp3<16>(hi, np, fam, sweeps, init, n_sv, st);
-      } else if (variant == 4) {   // two pairs per lane everywhere
-        launch_grp3<4>(lo, np, fam, sweeps, init, n_sv, st);
-        launch_grp3<8>(hi, np, fam, sweeps, init, n_sv, st);
-      } else {                     // default: measured best per regime
-        launch_v4<8>(lo, fam, sweeps, init, n_sv, st);
-        launch_grp3<8>(hi, np, fam, sweeps, init, n_sv, st);
-      }
-      return;
-    }
-    const int g = forced ? forced : (a.lanes ? a.lanes : 8);
-    if (g >= 32) launch_v4<32>(a, fam, sweeps, init, n_sv, st);
-    else if (g >= 16) launch_v4<16>(a, fam, sweeps, init, n_sv, st);
-    else launch_v4<8>(a, fam, sweeps, init, n_sv, st);
-    return;
-  }
-  if (!forced && !a.lanes && a.cells) {
-    SgmArgs lo = a, hi = a;
-    lo.select = 1;
-    hi.select = 2;
-    launch_grp<8>(lo, np, fam, sweeps, init, n_sv, st);
-    launch_grp<16>(hi, np, fam, sweeps, init, n_sv, st);
-    return;
-  }
-  const int g = forced ? forced : (a.lanes ? a.lanes : 8);
-  if (g >= 32) launch_grp<32>(a, np, fam, sweeps, init, n_sv, st);
-  else if (g >= 16) launch_grp<16>(a, np, fam, sweeps, init, n_sv, st);
-  else launch_grp<8>(a, np, fam, sweeps, init, n_sv, st);
-}
-
 template <class A, bool CF32>
 static void launch_family(const SgmArgs& a, int nch, int fam, int sweeps, int init, int n_sv,
                           cudaStream_t st) {
@@ -1450,11 +874,6 @@ void launch_aggregate(const SgmArgs& a, int arith, int n_sv, cudaStream_t st) {
     const int fams[4] = {FAM_H, FAM_V, FAM_D1, FAM_D2};
     const int widen = (n_sv <= 2 ? 2 : (n_sv <= 8 ? 1 : 0)) + (npairs_max(a.d_max) > 64);
     for (int k = 0; k < 4; ++k) launch_grp4_g(4 << widen, a, fams[k], k == 0, n_sv, st);
-  } else if (arith == ARITH_U16 && !v1) {
-    launch_family_seg(a, FAM_H, 3, 1, n_sv, st);
-    launch_family_seg(a, FAM_V, 3, 0, n_sv, st);
-    launch_family_seg(a, FAM_D1, 3, 0, n_sv, st);
-    launch_family_seg(a, FAM_D2, 3, 0, n_sv, st);
   } else if (arith == ARITH_U16) {
     launch_family<U16A, false>(a, nch, FAM_H, 3, 1, n_sv, st);
     launch_family<U16A, false>(a, nch, FAM_V, 3, 0, n_sv, st);
@@ -1550,12 +969,6 @@ __global__ void __launch_bounds__(256) k_wta_var(WtaArgs a) {
   a.r[o] = fmax((double)count, a.r_min);
 }
 
-// u16 sums, one thread per pixel: the argmin streams the pixel's pairs with
-// 8-byte loads where aligned, then walks outward (sgm.py:319-344).  The
-// pairs of neighbouring pixels are adjacent, so a warp's loads stay within a
-// few cache lines and the walk re-reads from L1.
-// variance walk + outputs of one pixel given its argmin key (value<<16 | d)
-// the pixel's pair rows of the (1..4) u16 partial sums
 template <int N>
 struct SumRows {
   const uint32_t* p[N];
@@ -1601,81 +1014,6 @@ __device__ __forceinline__ void wta_finish(const WtaArgs& a, const SumRows<N>& s
   a.dstar[o] = (uint16_t)dstar;
   a.valid[o] = dstar > 0;
   a.r[o] = fmax((double)count, a.r_min);
-}
-
-__device__ __forceinline__ bool wta_skip(const WtaArgs& a, int svl) {
-  if (!a.select) return false;
-  const double frac = (double)a.cells[svl] / ((double)a.W * a.H * (a.d_max + 1));
-  return (a.select == 1) == (frac > a.split);
-}
-
-constexpr int WTA_GRID = 64;   // blocks per (seq, view), grid-stride: early exits stay cheap
-
-template <int N>
-__global__ void __launch_bounds__(256) k_wta_var_u16(WtaArgs a) {
-  const size_t HW = (size_t)a.W * a.H;
-  const int svl = blockIdx.y;
-  if (wta_skip(a, svl)) return;
-  for (size_t pix = (size_t)blockIdx.x * blockDim.x + threadIdx.x; pix < HW;
-       pix += (size_t)gridDim.x * blockDim.x) {
-    const uint2 mt = a.meta[svl * HW + pix];
-    const int lo = lo_of(mt), hi = hi_of(mt);
-    const int j0 = lo >> 1, j1 = hi >> 1;
-    const SumRows<N> s = sum_rows<N>(a, svl * a.volcap + mt.y);
-    // key = value << 16 | d: the minimum key is the smallest value, then d
-    uint32_t best = 0xFFFFFFFFu;
-    {
-      const uint32_t w = s(0);
-      const uint32_t d0 = 2u * j0;
-      if ((int)d0 >= lo) best = min(best, ((w & 0xFFFFu) << 16) | d0);
-      if ((int)d0 + 1 <= hi) best = min(best, (w & 0xFFFF0000u) | (d0 + 1));
-    }
-    for (int j = j0 + 1; j < j1; ++j) {
-      const uint32_t w = s(j - j0);
-      const uint32_t d0 = 2u * j;
-      best = min(best, min(((w & 0xFFFFu) << 16) | d0, (w & 0xFFFF0000u) | (d0 + 1)));
-    }
-    if (j1 > j0) {
-      const uint32_t w = s(j1 - j0);
-      const uint32_t d0 = 2u * j1;
-      best = min(best, ((w & 0xFFFFu) << 16) | d0);
-      if ((int)d0 + 1 <= hi) best = min(best, (w & 0xFFFF0000u) | (d0 + 1));
-    }
-    wta_finish(a, s, lo, hi, j0, best, svl * HW + pix);
-  }
-}
-
-// u16 sums, 8 lanes per pixel: the group streams the pixel's pairs in
-// coalesced 32-byte rows, reduces (value << 16 | d) keys with shuffles, and
-// one lane walks outward from the winner over L1-resident data.
-template <int N>
-__global__ void __launch_bounds__(256) k_wta_var_u16g(WtaArgs a) {
-  const size_t HW = (size_t)a.W * a.H;
-  const int lane = threadIdx.x & 31;
-  const int gl = lane & 7;
-  const int svl = blockIdx.y;
-  if (wta_skip(a, svl)) return;   // block-uniform
-  const size_t stride = ((size_t)gridDim.x * blockDim.x) >> 3;
-  for (size_t pix = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
-       pix - ((threadIdx.x & 31) >> 3) < HW; pix += stride) {   // warp-uniform bound
-    const bool ok = pix < HW;
-    const uint2 mt = ok ? a.meta[svl * HW + pix] : make_uint2(0u, 0u);
-    const int lo = lo_of(mt), hi = hi_of(mt);
-    const int j0 = lo >> 1, j1 = hi >> 1;
-    const SumRows<N> s = sum_rows<N>(a, svl * a.volcap + mt.y);
-    uint32_t best = 0xFFFFFFFFu;
-    if (ok) {
-      for (int j = j0 + gl; j <= j1; j += 8) {
-        const uint32_t w = s(j - j0);
-        const uint32_t d0 = 2u * j;
-        if ((int)d0 >= lo) best = min(best, ((w & 0xFFFFu) << 16) | d0);
-        if ((int)d0 + 1 <= hi) best = min(best, (w & 0xFFFF0000u) | (d0 + 1));
-      }
-    }
-#pragma unroll
-    for (int o = 4; o; o >>= 1) best = min(best, __shfl_xor_sync(FULL, best, o));
-    if (ok && gl == 0) wta_finish(a, s, lo, hi, j0, best, svl * HW + pix);
-  }
 }
 
 // u16 sums, run-table schedule (as k_cost_runs): a warp owns 32 consecutive
@@ -1787,8 +1125,7 @@ __global__ void __launch_bounds__(WR_WARPS * 32) k_wta_runs(WtaArgs a, int rmax)
 }
 
 void launch_wta_variance(const WtaArgs& a, int n_sv, cudaStream_t st) {
-  static const bool runs = getenv("ES_WTA_OLD") == nullptr;   // A/B switch
-  if (runs && a.arith == ARITH_U16 && a.dstar_in == nullptr) {
+  if (a.arith == ARITH_U16 && a.dstar_in == nullptr) {
     const size_t HW = (size_t)a.W * a.H;
     const int nparts = 1 + (a.Sx[0] != nullptr) + (a.Sx[1] != nullptr) + (a.Sx[2] != nullptr);
     const int rmax = (npairs_max(a.d_max) + 3) / 4;
@@ -1809,30 +1146,6 @@ void launch_wta_variance(const WtaArgs& a, int n_sv, cudaStream_t st) {
     return;
   }
   const size_t HW = (size_t)a.W * a.H;
-  if (a.arith == ARITH_U16 && a.dstar_in == nullptr) {
-    const int nparts = 1 + (a.Sx[0] != nullptr) + (a.Sx[1] != nullptr) + (a.Sx[2] != nullptr);
-    // blocks per (seq, view): WTA_GRID, or enough that few large views still
-    // fill every SM (config 4: 16 views of 2048x1024)
-    const size_t per_sv = std::max<size_t>(WTA_GRID, (148 * 16 + n_sv - 1) / n_sv);
-    const unsigned g1 = (unsigned)std::min<size_t>((HW + 255) / 256, per_sv);
-    const unsigned g8 = (unsigned)std::min<size_t>((HW * 8 + 255) / 256, per_sv);
-    auto run = [&](auto thread_kernel, auto group_kernel) {
-      if (a.cells) {
-        WtaArgs lo = a, hi = a;
-        lo.select = 1;
-        hi.select = 2;
-        thread_kernel<<<dim3(g1, n_sv), 256, 0, st>>>(lo);
-        group_kernel<<<dim3(g8, n_sv), 256, 0, st>>>(hi);
-      } else {
-        thread_kernel<<<dim3(g1, n_sv), 256, 0, st>>>(a);
-      }
-    };
-    if (nparts == 1) run(k_wta_var_u16<1>, k_wta_var_u16g<1>);
-    else if (nparts == 2) run(k_wta_var_u16<2>, k_wta_var_u16g<2>);
-    else if (nparts == 3) run(k_wta_var_u16<3>, k_wta_var_u16g<3>);
-    else run(k_wta_var_u16<4>, k_wta_var_u16g<4>);
-    return;
-  }
   dim3 grid((unsigned)((HW + 7) / 8), n_sv);
   if (a.arith == ARITH_U16) k_wta_var<false><<<grid, 256, 0, st>>>(a);
   else k_wta_var<true><<<grid, 256, 0, st>>>(a);

@@ -620,7 +620,7 @@ struct Vec<4> {
 };
 
 template <int G, int NCH, int PPL, int MINB>
-__global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int fam, int init) {
+__global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int fam, int init, int sweeps) {
   constexpr int NG = 32 / G;
   constexpr int CW = PPL * G;      // pairs per chunk
   constexpr int NW = PPL * NCH;    // words per lane
@@ -766,19 +766,25 @@ __global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int
       s1 = s3;
     }
   };
+  // sweeps: bit 0 forward, bit 1 backward; the first sweep into a fresh
+  // partial sum (init) stores instead of accumulating
+  bool fresh = init != 0;
   for (int bwd = 0; bwd < 2; ++bwd) {
-    if (init && bwd == 0) sweep(bwd, std::false_type{});
+    if (!((sweeps >> bwd) & 1)) continue;
+    if (fresh) sweep(bwd, std::false_type{});
     else sweep(bwd, std::true_type{});
+    fresh = false;
   }
 }
 
 template <int G, int PPL, int MINB>
-static void launch_grp4(const SgmArgs& a, int fam, int init, int n_sv, cudaStream_t st) {
+static void launch_grp4(const SgmArgs& a, int fam, int init, int n_sv, cudaStream_t st,
+                        int sweeps = 3) {
   const int nchains = fam == FAM_H ? a.H : (fam == FAM_V ? a.W : a.W + a.H - 1);
   constexpr int per_block = G4_WARPS * (32 / G);
   dim3 grid((nchains + per_block - 1) / per_block, n_sv);
   const int nch = (npairs_max(a.d_max) + PPL * G - 1) / (PPL * G);
-  auto go = [&](auto kern) { kern<<<grid, G4_WARPS * 32, 0, st>>>(a, fam, init); };
+  auto go = [&](auto kern) { kern<<<grid, G4_WARPS * 32, 0, st>>>(a, fam, init, sweeps); };
   if (nch <= 1) go(k_sgm_grp4<G, 1, PPL, MINB>);
   else if (nch <= 2) go(k_sgm_grp4<G, 2, PPL, MINB>);
   else if (nch <= 4) go(k_sgm_grp4<G, 4, PPL, MINB>);
@@ -800,11 +806,12 @@ static void launch_family(const SgmArgs& a, int nch, int fam, int sweeps, int in
   }
 }
 
-static void launch_grp4_g(int G, const SgmArgs& a, int fam, int init, int n_sv, cudaStream_t st) {
-  if (G <= 4) launch_grp4<4, 4, 4>(a, fam, init, n_sv, st);
-  else if (G == 8) launch_grp4<8, 4, 1>(a, fam, init, n_sv, st);
-  else if (G == 16) launch_grp4<16, 4, 1>(a, fam, init, n_sv, st);
-  else launch_grp4<32, 4, 1>(a, fam, init, n_sv, st);
+static void launch_grp4_g(int G, const SgmArgs& a, int fam, int init, int n_sv, cudaStream_t st,
+                          int sweeps = 3) {
+  if (G <= 4) launch_grp4<4, 4, 4>(a, fam, init, n_sv, st, sweeps);
+  else if (G == 8) launch_grp4<8, 4, 1>(a, fam, init, n_sv, st, sweeps);
+  else if (G == 16) launch_grp4<16, 4, 1>(a, fam, init, n_sv, st, sweeps);
+  else launch_grp4<32, 4, 1>(a, fam, init, n_sv, st, sweeps);
 }
 
 // u16 aggregation with the per-(seq, view) kernel choice: sequences with
@@ -818,6 +825,34 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
   const int np = npairs_max(a.d_max);
   const int fams[4] = {FAM_H, FAM_V, FAM_D1, FAM_D2};
   static const int g4 = getenv("ES_SGM_G4") ? atoi(getenv("ES_SGM_G4")) : 1;   // A/B switch
+  // lanes per chain: G = 4 (8 chains per warp) fills the GPU from ~16 views
+  // up; smaller batches widen each chain so that enough warps are in flight,
+  // and D = 256 doubles G so the register-resident chunk arrays stay at <= 4
+  // words x 4 chunks (measured)
+  static const int widen_env = getenv("ES_SGM_WIDEN") ? atoi(getenv("ES_SGM_WIDEN")) : -1;
+  int widen = widen_env >= 0 ? widen_env : (n_sv <= 2 ? 2 : (n_sv <= 8 ? 1 : 0));
+  if (np > 64) widen += 1;
+  static const int split_env = getenv("ES_SGM_SPLITH") ? atoi(getenv("ES_SGM_SPLITH")) : 1;
+  if (g4 && parts == 4 && split_env) {
+    // small batches are latency-bound on the longest chain walk (a row's
+    // 2W steps): the row family's two sweeps run as separate jobs into their
+    // own partial sums, so the critical path is max(W, 3H) steps instead of
+    // 2W (jobs: S0 = rows ->, S1 = rows <-, S2 = columns + x-y diagonals ->,
+    // S3 = x-y diagonals <- + x+y diagonals)
+    struct Job { int part, fam, sweeps, init; };
+    const Job jobs[6] = {{0, FAM_H, 1, 1}, {1, FAM_H, 2, 1}, {2, FAM_V, 3, 1},
+                         {3, FAM_D1, 2, 1}, {2, FAM_D1, 1, 0}, {3, FAM_D2, 3, 0}};
+    for (const Job& j : jobs) {
+      SgmArgs lo = a, hi = a;
+      lo.select = 1;
+      hi.select = 2;
+      lo.S = S[j.part];
+      hi.S = S[j.part];
+      launch_grp4_g(4 << widen, lo, j.fam, j.init, n_sv, st_lo[j.part], j.sweeps);
+      launch_grp4_g(8 << widen, hi, j.fam, j.init, n_sv, st_hi[j.part], j.sweeps);
+    }
+    return;
+  }
   if (g4) {
     for (int k = 0; k < 4; ++k) {
       const int p = k % parts;
@@ -827,13 +862,6 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
       lo.S = S[p];
       hi.S = S[p];
       const int init = k < parts;
-      // lanes per chain: G = 4 (8 chains per warp) fills the GPU from ~16
-      // views up; smaller batches widen each chain so that enough warps are
-      // in flight, and D = 256 doubles G so the register-resident chunk
-      // arrays stay at <= 4 words x 4 chunks (measured)
-      static const int widen_env = getenv("ES_SGM_WIDEN") ? atoi(getenv("ES_SGM_WIDEN")) : -1;
-      int widen = widen_env >= 0 ? widen_env : (n_sv <= 2 ? 2 : (n_sv <= 8 ? 1 : 0));
-      if (np > 64) widen += 1;
       launch_grp4_g(4 << widen, lo, fams[k], init, n_sv, st_lo[p]);
       launch_grp4_g(8 << widen, hi, fams[k], init, n_sv, st_hi[p]);
     }

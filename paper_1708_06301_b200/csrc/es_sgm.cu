@@ -853,6 +853,26 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
     }
     return;
   }
+  static const int split2_env = getenv("ES_SGM_SPLIT2") ? atoi(getenv("ES_SGM_SPLIT2")) : 1;
+  if (g4 && parts == 2 && split2_env) {
+    // two partial sums: the row family's sweeps (the longest chains) run on
+    // both streams at once, so every stream carries one long and one short
+    // half: S0 = rows ->, columns, x+y diagonals ->; S1 = rows <-, x-y
+    // diagonals, x+y diagonals <-
+    struct Job { int part, fam, sweeps, init; };
+    const Job jobs[6] = {{0, FAM_H, 1, 1}, {1, FAM_H, 2, 1}, {0, FAM_V, 3, 0},
+                         {1, FAM_D1, 3, 0}, {0, FAM_D2, 1, 0}, {1, FAM_D2, 2, 0}};
+    for (const Job& j : jobs) {
+      SgmArgs lo = a, hi = a;
+      lo.select = 1;
+      hi.select = 2;
+      lo.S = S[j.part];
+      hi.S = S[j.part];
+      launch_grp4_g(4 << widen, lo, j.fam, j.init, n_sv, st_lo[j.part], j.sweeps);
+      launch_grp4_g(8 << widen, hi, j.fam, j.init, n_sv, st_hi[j.part], j.sweeps);
+    }
+    return;
+  }
   if (g4) {
     for (int k = 0; k < 4; ++k) {
       const int p = k % parts;

@@ -67,7 +67,7 @@ def use_config(n):
                     d_max=c["d_max"])
     g["SEQ_FRAMES"] = c["frames"]
 TEXTURE_SCALE = 0.05
-KERNELS_PER_STEP = 15   # zmax, zidx, fill_h, fill_v, cost, 4 families x 2 sgm variants, wta, fuse
+KERNELS_PER_STEP = 19   # zmax, zidx, fill_h, fill_v, cost, 6 sgm jobs x 2 regime variants, wta, fuse
 
 
 def measured_traffic(config, batch, texture_scale):

@@ -253,6 +253,9 @@ def main():
     ap.add_argument("--cpu-procs", type=int, default=default_cpu_procs())
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--full-range", action="store_true",
+                    help="PipelineParams(baseline=True): every frame full range (the config-1 "
+                         "workload per frame; tuning aid, not the headline)")
     ap.add_argument("--texture-scale", type=float, default=TEXTURE_SCALE,
                     help="world-space texture lattice (m); 0.05 gives paper-like ~50%% "
                          "search fractions, 0.2 gives ~10%%")
@@ -307,7 +310,8 @@ def main():
     specs = sequence_specs(B, seed0=seeds[0])
     frames = list(range(Wm + K))
     imgs = render_frames(specs, frames, device)
-    bp = pipeline.BatchedPipeline(rig, B, device=local)
+    bp = pipeline.BatchedPipeline(rig, B, pipeline.PipelineParams(baseline=args.full_range),
+                                  device=local)
     eng = bp.engine
     ext = torch.cuda.ExternalStream(eng.stream(), device=device)
 

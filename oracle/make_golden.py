@@ -422,8 +422,42 @@ def gen_kitti():
     save("kitti", **out)
 
 
+def gen_acceptance():
+    """Reference acceptance criteria on their own scenes: criterion 3 (10
+    rendered 32x32 scenes, full-range matcher == the independent brute-force
+    SGM of tests/reference_sgm.py) and criterion 4 (a 256x128 dolly-out
+    sequence: per-frame search fractions and the fused maps)."""
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    import helpers
+    import reference_sgm
+    out = {}
+    rig = helpers.make_rig(width=32, height=32, f=64.0, b=0.5, d_max=16)
+    prm = sgm.SgmParams()
+    for seed in range(10):
+        left, right, _, _ = synth.render_frame(helpers.small_scene(rig, texture_seed=seed), np.eye(4))
+        w, v = reference_sgm.match(left.data, right.data, rig.d_max, prm.window, prm.p1, prm.p2)
+        disp = sgm.select_disparity(sgm.aggregate_paths(
+            sgm.matching_cost(left, right, sgm.full_range_intervals(rig), prm), prm))
+        assert np.array_equal(disp.valid, v)
+        out[f"c3_{seed}_left"], out[f"c3_{seed}_right"] = left.data, right.data
+        out[f"c3_{seed}_winners"], out[f"c3_{seed}_valid"] = np.asarray(w), np.asarray(v)
+    rig = helpers.make_rig()   # 256x128, d_max = 64
+    frames = helpers.recede_sequence(rig, 10, step=0.1, texture_seed=7)
+    seq = pipeline.Sequence(rig=rig, lefts=[f.left for f in frames],
+                            rights=[f.right for f in frames],
+                            motions=[f.motion_exact for f in frames])
+    res = pipeline.run_sequence(seq, pipeline.PipelineParams())
+    for k, f in enumerate(frames):
+        out[f"c4_{k}_left"], out[f"c4_{k}_right"] = f.left.data, f.right.data
+        out[f"c4_{k}_motion"] = np.eye(4) if f.motion_exact is None else f.motion_exact
+        out[f"c4_{k}_fused_d"] = res[k].fused.left.values
+        out[f"c4_{k}_fused_v"] = res[k].fused.left.valid
+    out["c4_fractions"] = np.array([r.search_fraction_left for r in res])
+    save("acceptance", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["cost_agg", "misc", "prediction", "sequences", "config1", "metrics", "kitti"]
+    which = sys.argv[1:] or ["cost_agg", "misc", "prediction", "sequences", "config1", "metrics", "kitti", "acceptance"]
     if "cost_agg" in which:
         gen_cost_agg()
     if "misc" in which:
@@ -438,3 +472,5 @@ if __name__ == "__main__":
         gen_metrics()
     if "kitti" in which:
         gen_kitti()
+    if "acceptance" in which:
+        gen_acceptance()

@@ -452,6 +452,8 @@ def gen_acceptance():
         out[f"c4_{k}_motion"] = np.eye(4) if f.motion_exact is None else f.motion_exact
         out[f"c4_{k}_fused_d"] = res[k].fused.left.values
         out[f"c4_{k}_fused_v"] = res[k].fused.left.valid
+        for v, gt in (("l", f.gt_left), ("r", f.gt_right)):
+            out[f"c4_{k}_gt{v}_d"], out[f"c4_{k}_gt{v}_v"] = gt.values, gt.valid
     out["c4_fractions"] = np.array([r.search_fraction_left for r in res])
     save("acceptance", **out)
 

@@ -80,3 +80,69 @@ def test_criterion10_run_is_byte_deterministic(tmp_path):
     assert ta.keys() == tb.keys() and len(ta) >= 2 * n + 2
     for name in ta:
         assert ta[name] == tb[name], name
+
+
+def test_criterion8_ground_truth_inside_three_sigma():
+    """Criterion 8: on the dolly-out sequence, >= 95% of the predicted pixels
+    that are not occluded lie within +-3 sigma of the ground truth (the
+    non-occluded set: the previous ground truth warped by the exact motion
+    lands within 0.5 px of the current one)."""
+    from paper_1708_06301_b200 import core, pipeline, prediction
+    g = load_golden("acceptance")
+    rig = core.StereoRig(f=256.0, b=0.5, cx=127.5, cy=63.5, width=256, height=128, d_max=64)
+    n = len(g["c4_fractions"])
+    seq = pipeline.Sequence(
+        rig, [core.GrayImage(g[f"c4_{k}_left"]) for k in range(n)],
+        [core.GrayImage(g[f"c4_{k}_right"]) for k in range(n)],
+        [None] + [g[f"c4_{k}_motion"] for k in range(1, n)])
+    res = pipeline.run_sequence(seq, pipeline.PipelineParams())
+    prm = prediction.PredictionParams(q=0.0, edge_reject=False, fill_holes=False)
+    gt = lambda k, v: core.DisparityMap(g[f"c4_{k}_gt{v}_d"], g[f"c4_{k}_gt{v}_v"])   # noqa: E731
+    zero = core.VarianceMap(np.zeros((rig.height, rig.width)))
+    inside = total = 0
+    for k in range(1, n):
+        warped = prediction.predict_maps(core.FilterState(gt(k - 1, "l"), zero, gt(k - 1, "r"), zero,
+                                                          frame=k - 1), g[f"c4_{k}_motion"], rig, prm)
+        cur = gt(k, "l")
+        ok = warped.left.valid & cur.valid & (np.abs(warped.left.values - cur.values) <= 0.5)
+        mask = res[k].predicted_left.valid & ok
+        err = np.abs(res[k].predicted_left.values - cur.values)
+        band = 3.0 * np.sqrt(res[k].predicted_left_var.values)
+        inside += int((err[mask] <= band[mask]).sum())
+        total += int(mask.sum())
+    assert total > 1000 and inside / total >= 0.95
+
+
+def test_criterion7_flat_images_give_finite_variance_and_tie_break():
+    from paper_1708_06301_b200 import core, sgm
+    rig = core.StereoRig(f=64.0, b=0.5, cx=15.5, cy=15.5, width=32, height=32, d_max=16)
+    prm = sgm.SgmParams()
+    flat = core.GrayImage(np.full((32, 32), 100, np.uint8))
+    agg = sgm.aggregate_paths(sgm.matching_cost(flat, flat, sgm.full_range_intervals(rig), prm), prm)
+    disp = sgm.select_disparity(agg)
+    var = sgm.matching_variance_map(agg, disp, prm)
+    assert np.isfinite(var.values).all() and (var.values >= prm.r_min).all()
+    # ties resolve to the smaller disparity (sgm.py:282)
+    data = np.full((1, 1, 4), np.inf, np.float32)
+    data[0, 0] = [5.0, 2.0, 2.0, 7.0]
+    iv = sgm.IntervalMap(np.zeros((1, 1), np.int64), np.full((1, 1), 3, np.int64), 3)
+    assert sgm.select_disparity(sgm.CostVolume(data, iv)).values[0, 0] == 1.0
+
+
+def test_constant_shift_is_recovered_and_frame0_equals_baseline():
+    from paper_1708_06301_b200 import core, pipeline, sgm
+    rng = np.random.default_rng(13)
+    h, w, shift = 16, 48, 7
+    base = rng.integers(0, 256, (h, w + shift)).astype(np.uint8)
+    left, right = core.GrayImage(base[:, :w]), core.GrayImage(base[:, shift:])
+    rig = core.StereoRig(f=64.0, b=0.5, cx=(w - 1) / 2, cy=(h - 1) / 2, width=w, height=h, d_max=12)
+    prm = sgm.SgmParams()
+    disp = sgm.select_disparity(sgm.aggregate_paths(
+        sgm.matching_cost(left, right, sgm.full_range_intervals(rig), prm), prm))
+    assert (disp.values[2:-2, shift + 2:-2] == shift).all()
+    seq = pipeline.Sequence(rig, [left], [right], [None])
+    a = pipeline.run_sequence(seq, pipeline.PipelineParams())[0]
+    b = pipeline.run_sequence(seq, pipeline.PipelineParams(baseline=True))[0]
+    assert np.array_equal(a.fused.left.values, b.fused.left.values)
+    assert np.array_equal(a.fused.left.valid, b.fused.left.valid)
+    assert a.search_fraction_left == 1.0

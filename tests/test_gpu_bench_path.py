@@ -93,3 +93,40 @@ def test_e2e_host_inputs_async_exports_match_oracle():
             want = orc.step(host[k, s, 0], host[k, s, 1], specs[s][2][k])["left_fused"]
             enc = np.where(want[2], np.maximum(np.rint(want[0] * 256.0), 1.0), 0.0).astype(np.uint16)
             assert np.array_equal(outs[k].numpy().view(np.uint16)[s], enc), (s, k)
+
+
+@pytest.mark.slow
+def test_config5_full_batch_declared_subset_matches_oracle():
+    """The benchmark's exact configuration -- B = 64 sequences of 1242x375,
+    D = 128 in one context (two partial sums, split row sweeps, deferred
+    steps) -- with sequences {0, 21, 42, 63} checked against the oracle over
+    frames 0-2 (parity for config 5 on a declared subset)."""
+    import bench
+    from paper_1708_06301_b200 import core, pipeline
+    rig = core.StereoRig(**bench.RIG)
+    B, n = 64, 3
+    specs = bench.sequence_specs(B, seed0=1000)
+    imgs = bench.render_frames(specs, list(range(n)), "cuda:0")
+    bp = pipeline.BatchedPipeline(rig, B)
+    bp.process_frames(None, bench.motions_for(specs, 0), sync=True, images_dev=imgs[0].data_ptr())
+    for k in range(1, n):
+        bp.process_frames(None, bench.motions_for(specs, k), sync=False,
+                          images_dev=imgs[k].data_ptr())
+    bp.sync()
+    host = imgs.cpu().numpy()
+    for s in (0, 21, 42, 63):
+        orc = O.OracleStereo(rig.f, rig.b, rig.cx, rig.cy, rig.width, rig.height, rig.d_max)
+        for k in range(n):
+            want = orc.step(host[k, s, 0], host[k, s, 1], bench.motions_for(specs, k)[s])
+        got = bp.result(s)
+        for view, name in ((0, "left"), (1, "right")):
+            meas = got.measured_left if view == 0 else got.measured_right
+            assert np.array_equal(meas.values, want[name + "_meas"][0]), (s, name)
+            keep = got.keep_left if view == 0 else got.keep_right
+            assert np.array_equal(keep, want[name + "_keep"]), (s, name)
+            fd = got.fused.left if view == 0 else got.fused.right
+            fp = got.fused.left_var if view == 0 else got.fused.right_var
+            assert np.array_equal(fd.valid, want[name + "_fused"][2]), (s, name)
+            np.testing.assert_allclose(fd.values, want[name + "_fused"][0], rtol=1e-9, atol=0)
+            np.testing.assert_allclose(fp.values, want[name + "_fused"][1], rtol=1e-9, atol=0)
+        assert got.search_fraction_left < 1.0

@@ -148,3 +148,32 @@ def test_config4_full_size_batched_equals_single():
         assert got.search_fraction_left < 1.0
     finally:
         bench.use_config(5)
+
+
+@pytest.mark.slow
+def test_config3_full_size_moving_boxes_and_salt_noise():
+    """BASELINE config 3's features at the full 1242x375 size: three boxes
+    moving independently of the ego-motion and 2% salt noise per view, over
+    4 frames (fallback windows, LR rejection, adopt/drop), vs the oracle."""
+    import bench
+    from paper_1708_06301_b200 import core
+    rig = core.StereoRig(**bench.RIG)
+    n = 4
+    specs = bench.sequence_specs(1, seed0=3000)
+    boxes, poses, motions = specs[0][0], specs[0][1], specs[0][2]
+    rng = np.random.default_rng(303)
+    movers = [1, 4, 6]
+    vel = rng.uniform(-0.5, 0.5, (len(movers), 3)) * np.array([1.0, 0.0, 1.0])
+    per_frame = []
+    for k in range(n):
+        b = boxes.copy()
+        for i, bi in enumerate(movers):
+            b[bi, 0:2] += vel[i, 0] * k
+            b[bi, 4:6] += vel[i, 2] * k
+        per_frame.append(b)
+    frames = _render(rig, per_frame, poses[:n], seed=17, scale=bench.TEXTURE_SCALE)
+    for img in frames:
+        for v in range(2):
+            img[v][rng.random(img[v].shape) < 0.02] = 255
+    fr = _compare(rig, frames, motions[:n])
+    assert fr[0] == 1.0 and min(fr[1:]) < 1.0

@@ -388,7 +388,6 @@ def gen_kitti():
     """A KITTI-layout tree written by the reference (pipeline.write_sequence)
     and what the reference's load_sequence reads back from it."""
     import tempfile
-    from egostereo import kitti_io
     rig = rig_small(40, 24, 8, f=30.0, b=0.4)
     scene = synth.SceneSpec(rig=rig, primitives=(synth.Plane(z=3.0),), texture_seed=2)
     frames = synth.make_sequence(scene, synth.dolly_trajectory(3, -0.05), sigma_rot_deg=0.1,

@@ -2,8 +2,6 @@
 (metrics.py:39-117, pipeline.py:241-302) against outputs of the unmodified
 reference (tests/golden/metrics.npz, run_sequence.npz) and the oracle."""
 
-import os
-
 import numpy as np
 import pytest
 
@@ -73,7 +71,7 @@ def test_batched_device_metrics_match_host_metrics():
     host-map path on every sequence."""
     import torch
     import bench
-    from paper_1708_06301_b200 import _lib, core, metrics, pipeline
+    from paper_1708_06301_b200 import core, metrics, pipeline
     rig = core.StereoRig(f=180.0, b=0.54, cx=151.0, cy=46.0, width=310, height=94, d_max=40)
     B = 3
     specs = bench.sequence_specs(B, seed0=900)

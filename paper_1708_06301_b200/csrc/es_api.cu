@@ -334,6 +334,9 @@ int es_ctx_create(int device, const es_rig* rig, const es_params* prm, int batch
   int e = ES_OK;
   if (!e) e = dalloc(&c->img, n);
   if (!e) e = dalloc(&c->img2, n);
+  // KITTI export staging (2 slots): allocated here, never inside a step, so
+  // an export never triggers the implicit device synchronisation of cudaMalloc
+  if (!e) e = dalloc(&c->kitti, 2 * (size_t)batch * c->HW);
   for (int k = 0; k < 2 && !e; ++k) {
     e = dalloc(&c->sd[k], n);
     if (!e) e = dalloc(&c->sp[k], n);
@@ -788,7 +791,6 @@ extern "C" int es_ctx_export_all(es_ctx* c, int what, int view, void* out, int s
   if (what == ES_FUSED_KITTI) {
     // encode on the compute stream into one of two staging slots, copy out
     // on cp_out: the transfer overlaps the next step's kernels
-    if (!c->kitti) CK(cudaMalloc(&c->kitti, sizeof(uint16_t) * HW * B * 2));
     const int kb = c->kitti_slot;
     c->kitti_slot ^= 1;
     uint16_t* stage = c->kitti + (size_t)kb * HW * B;

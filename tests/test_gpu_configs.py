@@ -177,3 +177,18 @@ def test_config3_full_size_moving_boxes_and_salt_noise():
             img[v][rng.random(img[v].shape) < 0.02] = 255
     fr = _compare(rig, frames, motions[:n])
     assert fr[0] == 1.0 and min(fr[1:]) < 1.0
+
+
+@pytest.mark.parametrize("w,h,d_max", [(2, 2, 1), (3, 2, 2), (33, 2, 8), (40, 3, 39), (7, 64, 6), (64, 2, 63)])
+def test_degenerate_shapes_match_oracle(w, h, d_max):
+    """Edge shapes the reference accepts (at least 2x2, d_max < W): two-row
+    images, narrow column bands, d_max = W - 1, widths around a warp: two
+    frames (full range, then predicted under a small motion) vs the oracle."""
+    from paper_1708_06301_b200 import core
+    rig = core.StereoRig(f=float(max(w, 8)), b=0.5, cx=(w - 1) / 2.0, cy=(h - 1) / 2.0,
+                         width=w, height=h, d_max=d_max)
+    rng = np.random.default_rng(w * 100 + h)
+    frames = [rng.integers(0, 256, (2, h, w)).astype(np.uint8) for _ in range(2)]
+    frames[1][1] = np.roll(frames[1][0], -1, axis=1)   # some structure to match
+    motions = [None, core.make_motion(t=(0.01, 0.0, -0.02))]
+    _compare(rig, frames, motions)

@@ -130,3 +130,28 @@ def test_config5_full_batch_declared_subset_matches_oracle():
             np.testing.assert_allclose(fd.values, want[name + "_fused"][0], rtol=1e-9, atol=0)
             np.testing.assert_allclose(fp.values, want[name + "_fused"][1], rtol=1e-9, atol=0)
         assert got.search_fraction_left < 1.0
+
+
+@pytest.mark.parametrize("B", [1, 2, 5, 9])
+def test_every_batch_schedule_equals_single_sequences(B):
+    """Every aggregation schedule (4 partial sums with split row sweeps for
+    B <= 8, 2 partial sums for larger batches; lanes per chain widened for
+    small batches) gives each sequence exactly its single-sequence maps."""
+    import bench
+    from paper_1708_06301_b200 import core, pipeline, scenes
+    rig = core.StereoRig(f=180.0, b=0.54, cx=151.0, cy=46.0, width=310, height=94, d_max=40)
+    specs = [scenes.sequence_spec(seed=500 + s, n_frames=3, step=0.5, z_range=(4.0, 30.0))
+             for s in range(B)]
+    imgs = bench.render_frames(specs, [0, 1, 2], "cuda:0", rig=rig)
+    host = imgs.cpu().numpy()
+    bp = pipeline.BatchedPipeline(rig, B)
+    singles = [pipeline.DisparityPipeline(rig) for _ in range(B)]
+    for k in range(3):
+        bp.process_frames(None, [sp[2][k] for sp in specs], sync=True, images_dev=imgs[k].data_ptr())
+        for s in range(B):
+            want = singles[s].process_frame(core.GrayImage(host[k, s, 0]), core.GrayImage(host[k, s, 1]),
+                                            specs[s][2][k])
+            got = bp.result(s)
+            for a, b in ((want.measured_left, got.measured_left), (want.fused.right, got.fused.right)):
+                assert np.array_equal(a.values, b.values) and np.array_equal(a.valid, b.valid), (B, s, k)
+            assert np.array_equal(want.measured_right_var.values, got.measured_right_var.values)

@@ -143,12 +143,6 @@ __global__ void k_warp_points(const double* Hm, const double* pts, int n, double
   out[3 * i + 1] = yp;
   out[3 * i + 2] = dp;
 }
-__global__ void k_any_valid(const uint8_t* v, size_t HW, int* flag) {
-  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int sv = blockIdx.y;
-  bool any = i < HW && v[sv * HW + i];
-  if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) atomicOr(flag + (sv >> 1), 1);
-}
 
 }  // namespace
 

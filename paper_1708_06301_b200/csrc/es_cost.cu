@@ -229,12 +229,17 @@ __device__ __forceinline__ void cost_runs_row(const CostArgs& a, int rmax) {
       const bool fix = dbase < plo || dbase + 7 > phi || xm_far < 0 || xm_far > W - 1 ||
                        xm_near < 0 || xm_near > W - 1;
       if (__any_sync(FULL, fix)) {
+        // 8-bit masks over the run's cells: outside [lo, hi] (+inf wins) and
+        // match centre off the image (cells above a threshold, both views)
+        const int lo_c = max(plo - dbase, 0);
+        const int hi_c = min(phi - dbase, 7);
+        const int bt = min(max(sign < 0 ? px - dbase : W - 1 - px - dbase, -1), 7);
+        const uint32_t inv = ((1u << lo_c) - 1u) | (0xFFu & (0xFFu << (hi_c + 1)));
+        const uint32_t bor = 0xFFu & (0xFFu << (bt + 1));
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const int d = dbase + i;
-          const int xm = px + sign * d;
-          if ((unsigned)xm > (unsigned)(W - 1)) c[i] = border;
-          if (d < plo || d > phi) c[i] = INF16;
+          if ((bor >> i) & 1u) c[i] = border;
+          if ((inv >> i) & 1u) c[i] = INF16;
         }
       }
       if (live)

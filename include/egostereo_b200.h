@@ -108,7 +108,9 @@ enum {
 };
 int es_ctx_export(es_ctx* ctx, int what, int seq, int view, void* host_out);
 /* one map of one view for all `batch` sequences into host_out [batch][H][W]
- * (no dense volumes); sync = 0 only enqueues the copy on the context stream */
+ * (no dense volumes); sync = 0 only enqueues the work (ES_FUSED_KITTI: the
+ * encode on the context stream, the copy on the export stream -- see
+ * es_ctx_fence / es_ctx_sync); host_out must stay valid until then */
 int es_ctx_export_all(es_ctx* ctx, int what, int view, void* host_out, int sync);
 /* device pointer of a per-sequence map (what as above, no dense volumes) */
 int es_ctx_device_ptr(es_ctx* ctx, int what, int seq, int view, void** dev_ptr);

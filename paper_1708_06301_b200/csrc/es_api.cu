@@ -45,8 +45,10 @@ int check_rig(const es_rig* r) {
       r->height < 2)
     return fail(ES_ERR_VALUE, "invalid StereoRig");
   if (r->d_max > 511) return fail(ES_ERR_UNSUPPORTED, "device path supports d_max <= 511");
-  if ((double)row_capacity(r->width, r->d_max) * r->height >= 4294967295.0)
-    return fail(ES_ERR_UNSUPPORTED, "volume exceeds 2^32 pairs per view");
+  // pair offsets inside one view's volume are 32-bit; the aggregation forms
+  // signed per-lane bases from them
+  if ((double)row_capacity(r->width, r->d_max) * r->height >= 2147483647.0)
+    return fail(ES_ERR_UNSUPPORTED, "volume exceeds 2^31 pairs per view");
   return ES_OK;
 }
 

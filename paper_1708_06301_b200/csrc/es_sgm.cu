@@ -5,12 +5,20 @@
 // aggregate_paths), sgm.py:275-344 (select_disparity, matching_variance_map).
 //
 // Paths are independent chains of pixels: rows (H), columns (V), x-y = const
-// (D1) and x+y = const (D2).  One warp owns one chain and walks it; lane l
-// holds pair c*32 + l of chunk c (pair j = cells 2j, 2j+1) so a pixel's
-// interval touches only chunks (lo>>1)/32 .. (hi>>1)/32, a warp-uniform
-// range: reduced intervals cost one chunk per step, full range
-// ceil((d_max+1)/64).  The predecessor's values stay in registers; d-1 / d+1
-// neighbours come from one rotated shuffle each plus a byte permute.
+// (D1) and x+y = const (D2).  Kernels, in production order:
+//   k_sgm_grp4  (u16, production): a warp walks 32/G chains in lockstep, G
+//               lanes per chain, every lane owning one aligned 16-byte word
+//               (8 cells) of each absolute chunk; see its own comment and
+//               DESIGN.md section 4.  Launched as six jobs per step over two
+//               (or four) partial sums by launch_aggregate_parts.
+//   k_sgm_grp3  (u16): the previous production kernel, A/B baseline
+//               (ES_SGM_G4=0).
+//   k_sgm       (u16 / f32): one warp per chain, lane l holding pair
+//               c*32 + l of chunk c; the f32 path (non-integer penalties or
+//               arbitrary user volumes) and the per-direction launches in
+//               the reference's summation order use it.
+// Then k_wta_runs (u16 sums) / k_wta_var (f32 or caller winners) select the
+// disparity and walk the matching variance.
 //
 // Arithmetic policies:
 //   U16 (default integer penalties, small windows): two cells per 32-bit word,

@@ -533,12 +533,11 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   sa.p2i = c->prm.p2i;
   sa.p1 = c->prm.p1;
   sa.p2 = c->prm.p2;
-  // lanes per chain: wide intervals (large search fraction) favour 16 lanes,
-  // reduced ones 8 (measured); chosen per (seq, view) on the
-  // device from this frame's searched-cell count
+  // regime variants: each (seq, view) runs in the variant matching its
+  // search fraction, chosen on the device from this frame's searched-cell
+  // count (<= split: G lanes per chain, > split: 2G; measured)
   sa.lanes = c->lanes;
   sa.cells = c->cells;
-  // measured: the 4-lane kernel wins up to ~60% search fraction
   static const double split = getenv("ES_SGM_SPLIT") ? atof(getenv("ES_SGM_SPLIT")) : 0.6;
   sa.split = split;
   if (c->arith == ARITH_U16 && !c->lanes) {

@@ -63,10 +63,10 @@ struct SgmArgs {
   int cost_f32;
   uint32_t p1i, p2i;
   float p1, p2;
-  int lanes = 0;        // lanes per chain of the u16 kernel (8/16/32; 0 = default)
-  // device-side lane choice: with cells != nullptr both the 8- and 16-lane
-  // kernels launch and each (seq, view) runs in the one matching its search
-  // fraction (<= split: 8 lanes, > split: 16 lanes)
+  int lanes = 0;        // forced lanes per chain of the u16 kernel (0 = heuristic)
+  // device-side regime choice: with cells != nullptr both regime variants
+  // launch and each (seq, view) runs in the one matching its search fraction
+  // (<= split: narrow variant, > split: wide variant)
   const unsigned long long* cells = nullptr;
   double split = 0.3;
   int select = 0;       // internal: 0 all, 1 fraction <= split, 2 fraction > split
@@ -92,9 +92,7 @@ struct WtaArgs {
   uint8_t* valid;
   const uint16_t* dstar_in = nullptr;  // optional caller winners (variance only)
   const void* Sx[3] = {nullptr, nullptr, nullptr};  // further u16 partial sums (added to S)
-  // optional per-(seq, view) kernel choice as in SgmArgs: thread per pixel for
-  // reduced intervals, 8 lanes per pixel for wide ones
-  const unsigned long long* cells = nullptr;
+  const unsigned long long* cells = nullptr;   // unused by k_wta_runs
   int d_max = 0;
   double split = 0.3;
   int select = 0;

@@ -822,10 +822,11 @@ static void launch_grp4_g(int G, const SgmArgs& a, int fam, int init, int n_sv, 
   else launch_grp4<32, 4, 1>(a, fam, init, n_sv, st, sweeps);
 }
 
-// u16 aggregation with the per-(seq, view) kernel choice: sequences with
-// reduced intervals run the v4 kernel on st_lo, wide ones the 2-pairs/lane
-// kernel on st_hi; each (seq, view) is handled by exactly one stream, so the
-// two streams never touch the same volume and run concurrently
+// u16 aggregation with the per-(seq, view) regime choice: views with reduced
+// intervals run the narrow variant on st_lo[p], wide ones the wide variant on
+// st_hi[p]; each (seq, view) is handled by exactly one of them, so the two
+// never touch the same volume and run concurrently.  Jobs into the same
+// partial sum are ordered on its stream pair.
 void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S,
                             const cudaStream_t* st_lo, const cudaStream_t* st_hi) {
   // parts partial sums: family k accumulates into S[k % parts] on streams

@@ -834,12 +834,12 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
   const int np = npairs_max(a.d_max);
   const int fams[4] = {FAM_H, FAM_V, FAM_D1, FAM_D2};
   static const int g4 = getenv("ES_SGM_G4") ? atoi(getenv("ES_SGM_G4")) : 1;   // A/B switch
-  // lanes per chain: G = 4 (8 chains per warp) fills the GPU from ~16 views
-  // up; smaller batches widen each chain so that enough warps are in flight,
-  // and D = 256 doubles G so the register-resident chunk arrays stay at <= 4
-  // words x 4 chunks (measured)
+  // lanes per chain: G = 4 (8 chains per warp) from two sequences up -- the
+  // split job schedules keep enough warps in flight -- and G = 8 for a single
+  // sequence; D = 256 doubles G so the register-resident chunk arrays stay at
+  // <= 4 words x 4 chunks (measured)
   static const int widen_env = getenv("ES_SGM_WIDEN") ? atoi(getenv("ES_SGM_WIDEN")) : -1;
-  int widen = widen_env >= 0 ? widen_env : (n_sv <= 2 ? 2 : (n_sv <= 8 ? 1 : 0));
+  int widen = widen_env >= 0 ? widen_env : (n_sv <= 2 && np <= 64 ? 1 : 0);
   if (np > 64) widen += 1;
   static const int split_env = getenv("ES_SGM_SPLITH") ? atoi(getenv("ES_SGM_SPLITH")) : 1;
   if (g4 && parts == 4 && split_env) {

@@ -158,38 +158,76 @@ class StereoEngine:
         return s.value or 0
 
 
+# every map of one frame, as the device step left it: the engine, the
+# sequence, the step generation and the maps already read back
+_MAP_KEYS = ((_lib.ES_PRED_D, _lib.ES_PRED_VALID, _lib.ES_PRED_P, _lib.ES_LO, _lib.ES_HI,
+              _lib.ES_MEAS_D, _lib.ES_MEAS_VALID, _lib.ES_MEAS_R, _lib.ES_KEEP, _lib.ES_FUSED_D,
+              _lib.ES_FUSED_VALID, _lib.ES_FUSED_P))
+
+
+class _FrameMaps:
+    """Read-back cache of one frame's maps.  FrameResult and the lazy fused
+    state share it (neither references the other, so dropping both frees it
+    at once); the owning pipeline reads every map back before a later step
+    would overwrite them, if anything still holds the cache."""
+
+    def __init__(self, engine, seq):
+        self.engine = engine
+        self.seq = seq
+        self.gen = engine.generation
+        self.cache = {}
+
+    def get(self, what, view):
+        key = (what, view)
+        if key not in self.cache:
+            if self.engine.generation != self.gen:
+                raise RuntimeError("FrameResult maps were overwritten by a later frame")
+            self.cache[key] = self.engine.export(what, self.seq, view)
+        return self.cache[key]
+
+    def materialize(self):
+        for what in _MAP_KEYS:
+            for view in (0, 1):
+                self.get(what, view)
+
+
+class _LazyFilterState(FilterState):
+    """A FilterState whose maps are exported from the device on first access
+    (reading ``res.fused.left`` costs two device->host copies, not six)."""
+
+    def __init__(self, maps, frame):
+        object.__setattr__(self, "_maps", maps)
+        object.__setattr__(self, "frame", frame)
+
+    left = property(lambda s: DisparityMap(s._maps.get(_lib.ES_FUSED_D, 0),
+                                           s._maps.get(_lib.ES_FUSED_VALID, 0)))
+    left_var = property(lambda s: VarianceMap(s._maps.get(_lib.ES_FUSED_P, 0)))
+    right = property(lambda s: DisparityMap(s._maps.get(_lib.ES_FUSED_D, 1),
+                                            s._maps.get(_lib.ES_FUSED_VALID, 1)))
+    right_var = property(lambda s: VarianceMap(s._maps.get(_lib.ES_FUSED_P, 1)))
+
+
 class FrameResult:
     """Everything the pipeline derived for one frame (pipeline.py:53-72).
 
     Maps are read from the device on first access; the owning pipeline
     forces materialisation before its next step overwrites them."""
 
-    _FIELDS = ("predicted_left", "predicted_left_var", "predicted_right", "predicted_right_var",
-               "intervals_left", "intervals_right", "measured_left", "measured_left_var",
-               "measured_right", "measured_right_var", "keep_left", "keep_right", "fused")
-
     def __init__(self, engine: StereoEngine, seq: int, frame: int):
+        self._maps = _FrameMaps(engine, seq)
         self._engine = engine
-        self._seq = seq
-        self._gen = engine.generation
-        self._cache = {}
         self.frame = frame
+        self._fused = None
         l, r = engine.cells(seq)
         total = engine.rig.width * engine.rig.height * (engine.rig.d_max + 1)
         self.search_fraction_left = float(l / total)
         self.search_fraction_right = float(r / total)
 
     def _get(self, what, view):
-        key = (what, view)
-        if key not in self._cache:
-            if self._engine.generation != self._gen:
-                raise RuntimeError("FrameResult maps were overwritten by a later frame")
-            self._cache[key] = self._engine.export(what, self._seq, view)
-        return self._cache[key]
+        return self._maps.get(what, view)
 
     def materialize(self):
-        for name in self._FIELDS:
-            getattr(self, name)
+        self._maps.materialize()
         return self
 
     def _pred(self, v):
@@ -217,12 +255,11 @@ class FrameResult:
 
     @property
     def fused(self) -> FilterState:
-        return FilterState(
-            DisparityMap(self._get(_lib.ES_FUSED_D, 0), self._get(_lib.ES_FUSED_VALID, 0)),
-            VarianceMap(self._get(_lib.ES_FUSED_P, 0)),
-            DisparityMap(self._get(_lib.ES_FUSED_D, 1), self._get(_lib.ES_FUSED_VALID, 1)),
-            VarianceMap(self._get(_lib.ES_FUSED_P, 1)),
-            frame=self.frame)
+        """The posterior state (pipeline.py:64); its four maps are read from
+        the device one by one, on first access."""
+        if self._fused is None:
+            self._fused = _LazyFilterState(self._maps, self.frame)
+        return self._fused
 
     def cost_volume(self, view: int = 0) -> np.ndarray:
         """Dense export of the raw cost (parity / debugging)."""
@@ -276,7 +313,7 @@ class DisparityPipeline:
         self._img[0, 1] = R
         self._engine.step(self._img, [motion], sync=True)
         res = FrameResult(self._engine, 0, self._engine.frame(0))
-        self._last = weakref.ref(res)
+        self._last = weakref.ref(res._maps)
         return res
 
 

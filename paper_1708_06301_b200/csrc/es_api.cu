@@ -328,8 +328,10 @@ int es_ctx_create(int device, const es_rig* rig, const es_params* prm, int batch
   const size_t n = c->HW * 2 * batch;
   const size_t vol_words = c->volcap * 2 * batch * (c->arith == ARITH_F32 ? 2 : 1);
   int e = ES_OK;
-  if (!e) e = dalloc(&c->img, n);
-  if (!e) e = dalloc(&c->img2, n);
+  // image buffers carry 64 bytes of tail padding: the cost kernel stages
+  // rows with 16-byte-aligned bulk copies that may read past the last row
+  if (!e) e = dalloc(&c->img, n + 64);
+  if (!e) e = dalloc(&c->img2, n + 64);
   // KITTI export staging (2 slots): allocated here, never inside a step, so
   // an export never triggers the implicit device synchronisation of cudaMalloc
   if (!e) e = dalloc(&c->kitti, 2 * (size_t)batch * c->HW);
@@ -516,6 +518,8 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   ca.C = c->C;
   ca.volcap = c->volcap;
   ca.view0 = 0;
+  static const bool no_tma = getenv("ES_COST_NO_TMA") != nullptr;   // A/B switch
+  ca.tma = no_tma ? 0 : 1;
   launch_cost(ca, n_sv, c->st);
   CK(cudaEventRecord(c->ev_img_free[ib], c->st));   // the images' last reader
   mark(3);

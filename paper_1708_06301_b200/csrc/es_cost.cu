@@ -125,6 +125,13 @@ __host__ __device__ inline int cost_pad_cols(int d_max) { return ((d_max + 8) & 
 template <int SIGN>
 __device__ __forceinline__ void cost_runs_row(const CostArgs& a, int rmax);
 
+// byte offset of the TMA row buffers in the dynamic shared memory: after the
+// packed columns (words) and the run tables (bytes), 16-byte aligned
+__host__ __device__ inline size_t cost_rows_offset(int W, int padc, int rmax) {
+  const size_t cols = sizeof(uint32_t) * (2 * (size_t)W + 2 * (size_t)padc);
+  return (((cols + 15) & ~(size_t)15) + (size_t)CR_WARPS * 32 * rmax + 15) & ~(size_t)15;
+}
+
 __global__ void __launch_bounds__(CR_WARPS * 32) k_cost_runs(CostArgs a, int rmax) {
   // the match direction is a compile-time constant of each specialised body
   if (((a.view0 + (int)blockIdx.y) & 1) == 0) cost_runs_row<-1>(a, rmax);
@@ -150,13 +157,62 @@ __device__ __forceinline__ void cost_runs_row(const CostArgs& a, int rmax) {
   const uint2* meta = a.meta + (size_t)svl * HW + (size_t)y * W;
   const uint32_t rowbase = (uint32_t)(y * row_capacity(W, a.d_max));
   const int y0 = max(y - 1, 0), y2 = min(y + 1, H - 1);
-  for (int x = threadIdx.x; x < W; x += CR_WARPS * 32)
-    refcol[x] = (uint32_t)ref[(size_t)y0 * W + x] | ((uint32_t)ref[(size_t)y * W + x] << 8) |
-                ((uint32_t)ref[(size_t)y2 * W + x] << 16);
-  for (int k = threadIdx.x; k < W + 2 * PADC; k += CR_WARPS * 32) {
-    const int x = clampi(k - PADC, 0, W - 1);
-    othpad[k] = (uint32_t)oth[(size_t)y0 * W + x] | ((uint32_t)oth[(size_t)y * W + x] << 8) |
-                ((uint32_t)oth[(size_t)y2 * W + x] << 16);
+  if (a.tma) {
+    // TMA: the three rows of both images land in shared memory as byte rows
+    // by six bulk copies (16-byte-aligned supersets of the rows, one elected
+    // thread, one mbarrier); the packed columns are then built on chip
+    const int RS = (W + 31) & ~15;
+    uint8_t* rows = reinterpret_cast<uint8_t*>(sm) + cost_rows_offset(W, PADC, rmax);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(rows + 6 * (size_t)RS);
+    const uint8_t* src[6] = {ref + (size_t)y0 * W, ref + (size_t)y * W, ref + (size_t)y2 * W,
+                             oth + (size_t)y0 * W, oth + (size_t)y * W, oth + (size_t)y2 * W};
+    const unsigned bar_s = (unsigned)__cvta_generic_to_shared(bar);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t bytes = 0;
+      for (int r = 0; r < 6; ++r) {
+        const uintptr_t g = reinterpret_cast<uintptr_t>(src[r]);
+        bytes += (uint32_t)((((g & 15) + W) + 15) & ~(uintptr_t)15);
+      }
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s), "r"(bytes)
+                   : "memory");
+      for (int r = 0; r < 6; ++r) {
+        const uintptr_t g = reinterpret_cast<uintptr_t>(src[r]);
+        const uint32_t size = (uint32_t)((((g & 15) + W) + 15) & ~(uintptr_t)15);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"((unsigned)__cvta_generic_to_shared(rows + r * RS)), "l"(g & ~(uintptr_t)15),
+            "r"(size), "r"(bar_s) : "memory");
+      }
+    }
+    {
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}\n"
+                     : "=r"(done) : "r"(bar_s) : "memory");
+    }
+    const uint8_t* rr[6];
+    for (int r = 0; r < 6; ++r) rr[r] = rows + r * RS + (reinterpret_cast<uintptr_t>(src[r]) & 15);
+    for (int x = threadIdx.x; x < W; x += CR_WARPS * 32)
+      refcol[x] = (uint32_t)rr[0][x] | ((uint32_t)rr[1][x] << 8) | ((uint32_t)rr[2][x] << 16);
+    for (int k = threadIdx.x; k < W + 2 * PADC; k += CR_WARPS * 32) {
+      const int x = clampi(k - PADC, 0, W - 1);
+      othpad[k] = (uint32_t)rr[3][x] | ((uint32_t)rr[4][x] << 8) | ((uint32_t)rr[5][x] << 16);
+    }
+  } else {
+    for (int x = threadIdx.x; x < W; x += CR_WARPS * 32)
+      refcol[x] = (uint32_t)ref[(size_t)y0 * W + x] | ((uint32_t)ref[(size_t)y * W + x] << 8) |
+                  ((uint32_t)ref[(size_t)y2 * W + x] << 16);
+    for (int k = threadIdx.x; k < W + 2 * PADC; k += CR_WARPS * 32) {
+      const int x = clampi(k - PADC, 0, W - 1);
+      othpad[k] = (uint32_t)oth[(size_t)y0 * W + x] | ((uint32_t)oth[(size_t)y * W + x] << 8) |
+                  ((uint32_t)oth[(size_t)y2 * W + x] << 16);
+    }
   }
   __syncthreads();
   const uint32_t border = 9u * 255u;
@@ -254,8 +310,10 @@ void launch_cost(const CostArgs& a, int n_sv, cudaStream_t st) {
   if (a.window == 3) {
     const int rmax = (npairs_max(a.d_max) + 3) / 4;   // runs per pixel, at most
     dim3 grid(a.H, n_sv);
-    const size_t smem = sizeof(uint32_t) * (2 * (size_t)a.W + 2 * (size_t)cost_pad_cols(a.d_max)) +
-                        (size_t)CR_WARPS * 32 * rmax;
+    size_t smem = sizeof(uint32_t) * (2 * (size_t)a.W + 2 * (size_t)cost_pad_cols(a.d_max)) +
+                  (size_t)CR_WARPS * 32 * rmax;
+    if (a.tma)   // 16-byte-aligned byte rows + mbarrier
+      smem = cost_rows_offset(a.W, cost_pad_cols(a.d_max), rmax) + 6 * (size_t)((a.W + 31) & ~15) + 16;
     cudaFuncSetAttribute(k_cost_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_cost_runs<<<grid, CR_WARPS * 32, smem, st>>>(a, rmax);
     return;

@@ -47,6 +47,8 @@ struct CostArgs {
   uint32_t* C;          // [n_sv][volcap] u16 pairs
   size_t volcap;        // pairs per (seq, view)
   int view0;            // view of sv_local 0
+  int tma = 0;          // 1: img has >= 16 readable bytes past its end, so the
+                        //    image rows may be staged by 16-byte-aligned bulk copies
 };
 void launch_cost(const CostArgs& a, int n_sv, cudaStream_t st);
 

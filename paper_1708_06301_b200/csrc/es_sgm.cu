@@ -1083,7 +1083,7 @@ __device__ __forceinline__ void wta_finish(const WtaArgs& a, const SumRows<N>& s
 // L1-resident data.
 constexpr int WR_WARPS = 8;
 
-template <int N>
+template <int N, int U>
 __global__ void __launch_bounds__(WR_WARPS * 32) k_wta_runs(WtaArgs a, int rmax) {
   extern __shared__ uint32_t wsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1121,16 +1121,16 @@ __global__ void __launch_bounds__(WR_WARPS * 32) k_wta_runs(WtaArgs a, int rmax)
     for (int j = 0; j < nrun; ++j) tab[excl + j] = (uint8_t)lane;
     key[lane] = 0xFFFFFFFFu;
     __syncwarp();
-    // two runs per lane per iteration: all partial-sum loads of both are in
+    // U runs per lane per iteration: all partial-sum loads of them are in
     // flight before either is reduced; keys go to the pixel's slot with a
     // shared-memory atomicMin (ties resolve to the smaller d by the key)
-    for (int r0 = 0; r0 < total; r0 += 64) {
-      int p[2], plo[2], phi[2], pex[2];
-      uint32_t prun[2];
-      bool live[2];
-      uint4 w[2];
+    for (int r0 = 0; r0 < total; r0 += 32 * U) {
+      int p[U], plo[U], phi[U], pex[U];
+      uint32_t prun[U];
+      bool live[U];
+      uint4 w[U];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int r = r0 + 32 * u + lane;
         live[u] = r < total;
         p[u] = live[u] ? tab[r] : 31;
@@ -1151,7 +1151,7 @@ __global__ void __launch_bounds__(WR_WARPS * 32) k_wta_runs(WtaArgs a, int rmax)
         }
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < U; ++u) {
         if (!live[u]) continue;
         const int j = r0 + 32 * u + lane - pex[u];
         const uint32_t d0 = (uint32_t)((plo[u] & ~7) + 8 * j);
@@ -1196,10 +1196,20 @@ void launch_wta_variance(const WtaArgs& a, int n_sv, cudaStream_t st) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       kern<<<grid, WR_WARPS * 32, smem, st>>>(a, rmax);
     };
-    if (nparts == 1) go(k_wta_runs<1>);
-    else if (nparts == 2) go(k_wta_runs<2>);
-    else if (nparts == 3) go(k_wta_runs<3>);
-    else go(k_wta_runs<4>);
+    // runs in flight per lane: four for narrow views, two for wide ones
+    // (measured: 1242 px rows 3.49 -> 3.21 ms with four; 2048 px rows 4.75 ->
+    // 5.11 ms)
+    if (a.W <= 1536) {
+      if (nparts == 1) go(k_wta_runs<1, 4>);
+      else if (nparts == 2) go(k_wta_runs<2, 4>);
+      else if (nparts == 3) go(k_wta_runs<3, 4>);
+      else go(k_wta_runs<4, 4>);
+    } else {
+      if (nparts == 1) go(k_wta_runs<1, 2>);
+      else if (nparts == 2) go(k_wta_runs<2, 2>);
+      else if (nparts == 3) go(k_wta_runs<3, 2>);
+      else go(k_wta_runs<4, 2>);
+    }
     return;
   }
   const size_t HW = (size_t)a.W * a.H;

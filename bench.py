@@ -19,6 +19,8 @@ e2e        the same through the public API (BatchedPipeline.process_frames)
            (KITTI uint16) of every sequence copied out each step
 roofline   aggregation stage (4 SGM family launches): algorithmic bytes
            4*N_v + 8*HW per view / CUDA-event stage time
+roofline_int  the same stage on the ALU pipe (8 u16 ops per cell and path
+           direction, u16x2 packed): its binding roofline
 cpu_baseline  the numpy oracle port on the host, one predicted frame per
            process, P processes in parallel
 """
@@ -82,6 +84,42 @@ def measured_traffic(config, batch, texture_scale):
     except Exception:
         pass
     return None
+
+
+def measured_alu(config, batch, texture_scale):
+    """ncu ALU-pipe utilisation (%) of the aggregation launches in the same
+    committed capture, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "agg_traffic.json")) as fh:
+            t = json.load(fh)
+        if (t.get("config", 5) == config and t["batch"] == batch
+                and abs(t["texture_scale"] - texture_scale) < 1e-12):
+            return float(t["alu_pipe_active_pct"])
+    except Exception:
+        pass
+    return None
+
+
+# Integer roofline of the aggregation (SURVEY 8(d): its arithmetic intensity
+# sits above the INT/HBM ridge).  Per searched cell and path direction the
+# recurrence L = C + min(Lp(d), min(Lp(d-1), Lp(d+1)) + P1, m + P2) - m costs
+# 8 u16 operations (3 min, +P1, -m, +C, the running min for m, the add into
+# the path sum); u16x2 packs two per lane instruction on the ALU pipe, which
+# retires 64 lanes per clock per SM (B300_MICROARCH.md: rt_SMSP = 2).
+AGG_OPS_PER_CELL_DIR = 8
+ALU_LANES_PER_SM_CLK = 64
+
+
+def alu_roofline(cells, ms, sm_mhz, n_sm, alu_pct):
+    ops = 8 * AGG_OPS_PER_CELL_DIR * cells
+    peak = n_sm * ALU_LANES_PER_SM_CLK * 2 * sm_mhz * 1e6 / 1e12
+    achieved = ops / (ms / 1e3) / 1e12
+    return {"bound": "alu", "ops_per_step": ops, "ops_per_cell_direction": AGG_OPS_PER_CELL_DIR,
+            "achieved": achieved, "peak": peak, "unit": "Tops/s (u16)", "frac": achieved / peak,
+            "floor_ms": ops / (peak * 1e12) * 1e3,
+            "peak_basis": f"{n_sm} SMs x {ALU_LANES_PER_SM_CLK} ALU lanes/clk x 2 u16 per lane "
+                          f"x {sm_mhz:.0f} MHz (median SM clock under load)",
+            "ncu_alu_pipe_active_pct": alu_pct}
 
 
 def stage_roofline(nbytes, ms, peak):
@@ -424,11 +462,17 @@ def main():
                      # this workload), vs bytes_per_step algorithmic
                      "traffic": measured_traffic(args.config, B, TEXTURE_SCALE),
                      "traffic_unit": "bytes per step (all sequences, both views)",
-                     "peak_kind": peak_kind, "bytes_per_step": agg_bytes},
+                     "peak_kind": peak_kind, "bytes_per_step": agg_bytes,
+                     "floor_ms": agg_bytes / (peak * 1e9) * 1e3},
         # the multi-pass aggregation reads C and read-modify-writes a partial
         # sum once per direction: its DRAM traffic / stage time is the
         # bandwidth it actually sustains
         "aggregation_dram": traffic_line(measured_traffic(args.config, B, TEXTURE_SCALE), agg_ms, peak),
+        # the same stage against the integer pipe: its HBM floor (bytes_per_step
+        # / peak) is below its ALU floor, so the ALU pipe is the binding roofline
+        "roofline_int": alu_roofline(cells, agg_ms, (clk or {}).get("sm_mhz") or 1965.0,
+                                     torch.cuda.get_device_properties(device).multi_processor_count,
+                                     measured_alu(args.config, B, TEXTURE_SCALE)),
         # the other SURVEY 8(d) kernels on their algorithmic bytes
         "roofline_stages": {
             "cost": stage_roofline(2 * hw * 2 * B + 8 * hw * 2 * B + 2 * cells,

@@ -221,11 +221,6 @@ struct es_ctx {
   unsigned long long* cells_acc = nullptr;   // searched cells summed over steps
   int lanes = 0;               // SGM lanes per chain (0 = heuristic)
   double last_fraction = 1.0;  // search fraction of the last synced step
-  // wavefront SGM jobs (ES_SGM_WAVE=1, two partial sums): per pass a record
-  // ring and progress flags, zeroed before every aggregation
-  uint32_t* wave_ring[2] = {nullptr, nullptr};
-  unsigned* wave_flags[2] = {nullptr, nullptr};
-  size_t wave_flag_n = 0;
 
   void note_fraction() {
     unsigned long long cells = 0;
@@ -244,8 +239,7 @@ int ctx_free(es_ctx* c) {
                   c->C, c->S,
                   c->Sx[0], c->Sx[1], c->Sx[2], c->dstar, c->r, c->mvalid, c->keep, c->Hm,
                   c->have_pred, c->err, c->anyv,
-                  c->cells, c->kitti, c->cells_acc, c->img2, c->wave_ring[0], c->wave_ring[1],
-                  c->wave_flags[0], c->wave_flags[1]};
+                  c->cells, c->kitti, c->cells_acc, c->img2};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   void* hptrs[] = {c->h_Hm, c->h_have, c->h_err, c->h_anyv, c->h_cells};
@@ -366,15 +360,6 @@ int es_ctx_create(int device, const es_rig* rig, const es_params* prm, int batch
     c->parts = pe ? atoi(pe) : (batch <= 8 ? 4 : 2);
     if (c->parts != 1 && c->parts != 2 && c->parts != 4) c->parts = 2;
     for (int p = 0; p + 1 < c->parts && !e; ++p) e = dalloc(&c->Sx[p], vol_words);
-    const char* we = getenv("ES_SGM_WAVE");
-    if (!e && we && atoi(we) && c->parts == 2 && wave_supported(c->rig.d_max)) {
-      const int n_sv = 2 * batch;
-      c->wave_flag_n = wave_flag_words(c->rig.W, n_sv);
-      for (int k = 0; k < 2 && !e; ++k) {
-        e = dalloc(&c->wave_ring[k], wave_ring_words(c->rig.W, c->rig.H, n_sv));
-        if (!e) e = dalloc(&c->wave_flags[k], c->wave_flag_n);
-      }
-    }
   }
   if (!e) e = dalloc(&c->dstar, n);
   if (!e) e = dalloc(&c->r, n);
@@ -566,13 +551,6 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
     void* S[4] = {c->S, c->Sx[0], c->Sx[1], c->Sx[2]};
     const cudaStream_t lo[4] = {c->st, c->sx[1], c->sx[3], c->sx[5]};
     const cudaStream_t hi[4] = {c->sx[0], c->sx[2], c->sx[4], c->sx[6]};
-    if (c->wave_ring[0]) {
-      for (int k = 0; k < 2; ++k) {
-        CK(cudaMemsetAsync(c->wave_flags[k], 0, sizeof(unsigned) * c->wave_flag_n, c->st));
-        sa.wave_ring[k] = c->wave_ring[k];
-        sa.wave_flags[k] = c->wave_flags[k];
-      }
-    }
     CK(cudaEventRecord(c->ev_fork, c->st));
     for (int p = 0; p < P; ++p) {
       if (p) CK(cudaStreamWaitEvent(lo[p], c->ev_fork, 0));

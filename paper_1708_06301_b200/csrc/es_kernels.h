@@ -72,16 +72,7 @@ struct SgmArgs {
   const unsigned long long* cells = nullptr;
   double split = 0.3;
   int select = 0;       // internal: 0 all, 1 fraction <= split, 2 fraction > split
-  // wavefront jobs (k_sgm_wave): per pass, a column-edge record ring and
-  // per-lane progress flags (zeroed before the pass)
-  uint32_t* wave_ring[2] = {nullptr, nullptr};
-  unsigned* wave_flags[2] = {nullptr, nullptr};
 };
-// wavefront aggregation (columns + one diagonal per pass): usable for
-// d_max <= 127; ring words and flag words per context for n_sv views
-size_t wave_ring_words(int W, int H, int n_sv);
-size_t wave_flag_words(int W, int n_sv);
-bool wave_supported(int d_max);
 // full 8-path aggregation; the u16 path runs 4 family launches (both sweeps
 // each), the f32 path runs the 8 directions in the reference's order
 void launch_aggregate(const SgmArgs& a, int arith, int n_sv, cudaStream_t st);

@@ -822,265 +822,6 @@ static void launch_grp4_g(int G, const SgmArgs& a, int fam, int init, int n_sv, 
   else launch_grp4<32, 4, 1>(a, fam, init, n_sv, st, sweeps);
 }
 
-// ------------------------------------------------------------ wavefront (u16)
-//
-// Column + diagonal paths in one row sweep.  A warp owns a strip of NG = 32/G
-// adjacent columns (G lanes per column, the grp4 word layout) and walks the
-// rows; per row it updates the column path (its own registers) and one
-// diagonal path whose predecessor is the neighbouring column of the previous
-// row: inside the warp that state moves one lane group per row by shuffles,
-// across strips it is handed over through a global record ring with
-// per-lane release/acquire progress flags.  Strips run as a wavefront in the
-// diagonal's direction (lower block index = upstream strip, so a waiting
-// strip's producer is always resident or finished).  One read of C and one
-// read-modify-write of the partial sum serve two path directions.
-//   down pass (UP = 0): rows 0 -> H-1, paths (0,+1) and (+1,+1): predecessor
-//                       (x, y-1) and (x-1, y-1), wavefront left -> right;
-//   up pass   (UP = 1): rows H-1 -> 0, paths (0,-1) and (-1,-1): predecessor
-//                       (x, y+1) and (x+1, y+1), wavefront right -> left.
-// The remaining directions (+-1, 0) and the x+y diagonals run in grp4 jobs.
-constexpr int WAVE_G = 8, WAVE_PPL = 4, WAVE_NCH = 2, WAVE_WARPS = 4;
-constexpr int WAVE_NW = WAVE_PPL * WAVE_NCH;            // words per lane
-constexpr int WAVE_LREC = WAVE_NW + 4;                  // words per lane record (data, mp2, ng, pad)
-constexpr int WAVE_REC = WAVE_G * WAVE_LREC;            // words per (strip, row)
-
-__host__ __device__ inline int wave_strips(int W) { return (W + 32 / WAVE_G - 1) / (32 / WAVE_G); }
-size_t wave_ring_words(int W, int H, int n_sv) {
-  return (size_t)n_sv * wave_strips(W) * H * WAVE_REC;
-}
-size_t wave_flag_words(int W, int n_sv) { return (size_t)n_sv * wave_strips(W) * WAVE_G; }
-bool wave_supported(int d_max) { return npairs_max(d_max) <= WAVE_PPL * WAVE_G * WAVE_NCH; }
-
-template <bool UP>
-__global__ void __launch_bounds__(WAVE_WARPS * 32, 4) k_sgm_wave(SgmArgs a) {
-  constexpr int G = WAVE_G, PPL = WAVE_PPL, NCH = WAVE_NCH, NW = WAVE_NW;
-  constexpr int NG = 32 / G;
-  constexpr int CW = PPL * G;
-  constexpr uint32_t NONE = 0xFFFFFFFFu;
-  const int lane = threadIdx.x & 31;
-  const int gl = lane & (G - 1);
-  const int grp = lane / G;
-  const int gbase = lane & ~(G - 1);
-  const int W = a.W, H = a.H;
-  const int nstrips = wave_strips(W);
-  const int wi = blockIdx.x * WAVE_WARPS + (threadIdx.x >> 5);   // wavefront order
-  if (wi >= nstrips) return;
-  if (a.select) {
-    const double frac = (double)a.cells[blockIdx.y] / ((double)W * H * (a.d_max + 1));
-    if ((a.select == 1) == (frac > a.split)) return;
-  }
-  const int strip = UP ? nstrips - 1 - wi : wi;
-  const int x = strip * NG + grp;
-  const size_t HW = (size_t)W * H;
-  const uint2* __restrict__ meta = a.meta + (size_t)blockIdx.y * HW;
-  const uint32_t* __restrict__ C =
-      reinterpret_cast<const uint32_t*>(a.C) + (size_t)blockIdx.y * a.volcap;
-  uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
-  asm volatile("" : "+l"(C));
-  asm volatile("" : "+l"(S));
-  // edge hand-over: the producer group is the strip's downstream edge, the
-  // consumer group its upstream edge
-  const bool producer = UP ? grp == 0 : grp == NG - 1;
-  const bool consumer = UP ? grp == NG - 1 : grp == 0;
-  const int up_strip = UP ? strip + 1 : strip - 1;
-  const bool has_in = up_strip >= 0 && up_strip < nstrips;
-  const size_t vs = (size_t)blockIdx.y * nstrips;
-  uint32_t* ring = a.wave_ring[UP];
-  unsigned* flags = a.wave_flags[UP];
-  uint32_t* rec_out = ring + ((vs + strip) * H) * WAVE_REC + gl * WAVE_LREC;
-  const uint32_t* rec_in = ring + ((vs + (has_in ? up_strip : strip)) * H) * WAVE_REC + gl * WAVE_LREC;
-  unsigned* flag_out = flags + (vs + strip) * G + gl;
-  const unsigned* flag_in = flags + (vs + (has_in ? up_strip : strip)) * G + gl;
-
-  const int src_l = gbase | ((gl + G - 1) & (G - 1));
-  const int src_r = gbase | ((gl + 1) & (G - 1));
-  auto umask = [](int lo, int hi) -> uint32_t {
-    return hi < lo ? 0u : ((hi >= 31 ? 0xFFFFFFFFu : ((2u << hi) - 1u)) & ~((1u << lo) - 1u));
-  };
-  auto load_meta = [&](int t) -> uint2 {
-    if (t < H && x < W) {
-      const int y = UP ? H - 1 - t : t;
-      return meta[(size_t)y * W + x];
-    }
-    return make_uint2(NONE, 0u);
-  };
-  auto info = [&](uint2 mt) -> G4Step {
-    G4Step s{0, 0, 0u, 0u};
-    int clo = NCH, chi = -1;
-    if (mt.x != NONE) {
-      const int j0 = (int)((mt.x & 0xFFFFu) >> 1);
-      const int j1 = (int)((mt.x >> 16) >> 1);
-      s.base = (int)(mt.y - (uint32_t)j0) + PPL * gl;
-      s.relb = PPL * gl - j0 + PPL - 1;
-      s.spanp = (uint32_t)(j1 - j0 + PPL);
-      clo = j0 / CW;
-      chi = j1 / CW;
-    }
-    s.um = umask(__reduce_min_sync(FULL, clo), __reduce_max_sync(FULL, chi));
-    return s;
-  };
-  auto pred_of = [&](const G4Step& s, int c) -> bool {
-    return (uint32_t)(s.relb + c * CW) < s.spanp;
-  };
-  auto fetch = [&](const G4Step& s, uint32_t (&cn)[NW], uint32_t (&sn)[NW], int c) {
-    const bool p = pred_of(s, c);
-    Vec<PPL>::ldc(C + s.base + c * CW, p, &cn[c * PPL]);
-    Vec<PPL>::ld_any(S + s.base + c * CW, p, &sn[c * PPL]);
-  };
-  uint32_t pv[NW], pd[NW], cA[NW], sA[NW], cB[NW], sB[NW];
-  uint2 mA = load_meta(0), mB = load_meta(1);
-  G4Step s0 = info(mA);
-  G4Step s1 = info(mB);
-  mA = load_meta(2);
-  mB = load_meta(3);
-#pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-#pragma unroll
-    for (int k = 0; k < PPL; ++k) pv[c * PPL + k] = pd[c * PPL + k] = INF16x2;
-    fetch(s0, cA, sA, c);
-    fetch(s1, cB, sB, c);
-  }
-  uint32_t mv = INF16x2, nv = INF16x2;   // column path: m + P2, -m (none: L = C)
-  uint32_t md = INF16x2, nd = INF16x2;   // diagonal path, of this group's column
-  const uint32_t p1x2 = a.p1i * 0x10001u;
-  // one path update of chunk c from the predecessor words P (grp4 body)
-  auto path = [&](const uint32_t (&P)[PPL], uint32_t pl, uint32_t pr, uint32_t mp2, uint32_t ng,
-                  const uint32_t* cn, uint32_t (&L)[PPL]) {
-    uint32_t X[PPL + 1];
-    X[0] = __byte_perm(pl, P[0], 0x5432);
-#pragma unroll
-    for (int k = 1; k < PPL; ++k) X[k] = __byte_perm(P[k - 1], P[k], 0x5432);
-    X[PPL] = __byte_perm(P[PPL - 1], pr, 0x5432);
-#pragma unroll
-    for (int k = 0; k < PPL; ++k) {
-      const uint32_t cand = __viaddmin_u16x2(__vminu2(X[k], X[k + 1]), p1x2, __vminu2(P[k], mp2));
-      L[k] = __vadd2(cn[k], __vadd2(cand, ng));
-    }
-  };
-  auto step = [&](const int t, const G4Step& cur, const G4Step& nn, uint32_t (&cn)[NW],
-                  uint32_t (&sn)[NW]) {
-    // diagonal predecessor: the neighbouring group's column, one group
-    // along the wavefront; the upstream edge group takes the upstream
-    // strip's record of the previous row
-#pragma unroll
-    for (int k = 0; k < NW; ++k)
-      pd[k] = UP ? __shfl_down_sync(FULL, pd[k], G) : __shfl_up_sync(FULL, pd[k], G);
-    md = UP ? __shfl_down_sync(FULL, md, G) : __shfl_up_sync(FULL, md, G);
-    nd = UP ? __shfl_down_sync(FULL, nd, G) : __shfl_up_sync(FULL, nd, G);
-    if (consumer) {
-      if (has_in && t > 0) {
-        unsigned f;
-        for (;;) {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(flag_in) : "memory");
-          if (f >= (unsigned)t) break;
-#ifdef ES_WAVE_SLEEP
-          __nanosleep(ES_WAVE_SLEEP);
-#endif
-        }
-        const uint32_t* r = rec_in + (size_t)(t - 1) * WAVE_REC;
-        uint32_t e[NW + 4];
-#pragma unroll
-        for (int q = 0; q < NW + 4; q += 4) {
-          asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(e[q]), "=r"(e[q + 1]), "=r"(e[q + 2]), "=r"(e[q + 3])
-                       : "l"(r + q) : "memory");
-        }
-#pragma unroll
-        for (int k = 0; k < NW; ++k) pd[k] = e[k];
-        md = e[NW];
-        nd = e[NW + 1];
-      } else {
-#pragma unroll
-        for (int k = 0; k < NW; ++k) pd[k] = INF16x2;
-        md = nd = INF16x2;   // off-image predecessor: restart
-      }
-    }
-    __syncwarp();
-    uint32_t vmin = INF16x2, dmin = INF16x2;
-    uint32_t lv_old = INF16x2, ld_old = INF16x2;
-    uint32_t* Sb = S + cur.base;
-#pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-      uint32_t PV[PPL], PD[PPL];
-#pragma unroll
-      for (int k = 0; k < PPL; ++k) {
-        PV[k] = pv[c * PPL + k];
-        PD[k] = pd[c * PPL + k];
-      }
-      if ((cur.um >> c) & 1u) {
-        const int cn1 = c + 1 < NCH ? c + 1 : 0;
-        const uint32_t vsl = gl == G - 1 ? lv_old : PV[PPL - 1];
-        const uint32_t vsr = gl == 0 ? (c + 1 < NCH ? pv[cn1 * PPL] : INF16x2) : PV[0];
-        const uint32_t dsl = gl == G - 1 ? ld_old : PD[PPL - 1];
-        const uint32_t dsr = gl == 0 ? (c + 1 < NCH ? pd[cn1 * PPL] : INF16x2) : PD[0];
-        const uint32_t vl = __shfl_sync(FULL, vsl, src_l), vr = __shfl_sync(FULL, vsr, src_r);
-        const uint32_t dl = __shfl_sync(FULL, dsl, src_l), dr = __shfl_sync(FULL, dsr, src_r);
-        uint32_t LV[PPL], LD[PPL], Ssum[PPL];
-        path(PV, vl, vr, mv, nv, &cn[c * PPL], LV);
-        path(PD, dl, dr, md, nd, &cn[c * PPL], LD);
-#pragma unroll
-        for (int k = 0; k < PPL; ++k) {
-          Ssum[k] = __vadd2(sn[c * PPL + k], __vadd2(LV[k], LD[k]));
-          pv[c * PPL + k] = LV[k];
-          pd[c * PPL + k] = LD[k];
-        }
-        vmin = __vimin3_u16x2(vmin, LV[0], LV[1]);
-        vmin = __vimin3_u16x2(vmin, LV[2], LV[3]);
-        dmin = __vimin3_u16x2(dmin, LD[0], LD[1]);
-        dmin = __vimin3_u16x2(dmin, LD[2], LD[3]);
-        Vec<PPL>::st(Sb + c * CW, pred_of(cur, c), Ssum);
-      } else {
-#pragma unroll
-        for (int k = 0; k < PPL; ++k) pv[c * PPL + k] = pd[c * PPL + k] = INF16x2;
-      }
-      lv_old = PV[PPL - 1];
-      ld_old = PD[PPL - 1];
-      if ((nn.um >> c) & 1u) fetch(nn, cn, sn, c);
-    }
-    uint32_t hv = min(vmin & 0xFFFFu, vmin >> 16);
-    uint32_t hd = min(dmin & 0xFFFFu, dmin >> 16);
-#pragma unroll
-    for (int o = G / 2; o; o >>= 1) {
-      hv = min(hv, __shfl_xor_sync(FULL, hv, o));
-      hd = min(hd, __shfl_xor_sync(FULL, hd, o));
-    }
-    const bool act = cur.spanp != 0u;
-    mv = act ? (hv + a.p2i) * 0x10001u : INF16x2;
-    nv = act ? ((0x10000u - hv) & 0xFFFFu) * 0x10001u : INF16x2;
-    md = act ? (hd + a.p2i) * 0x10001u : INF16x2;
-    nd = act ? ((0x10000u - hd) & 0xFFFFu) * 0x10001u : INF16x2;
-    if (producer) {
-      // this row's diagonal state of the downstream edge column, then the
-      // lane's progress flag (release: orders the record before it)
-      uint32_t* r = rec_out + (size_t)t * WAVE_REC;
-#pragma unroll
-      for (int q = 0; q < NW; q += 4)
-        asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};"
-                     :: "l"(r + q), "r"(pd[q]), "r"(pd[q + 1]), "r"(pd[q + 2]), "r"(pd[q + 3]) : "memory");
-      asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};"
-                   :: "l"(r + NW), "r"(md), "r"(nd), "r"(0u), "r"(0u) : "memory");
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(flag_out), "r"((unsigned)(t + 1)) : "memory");
-    }
-  };
-  for (int t = 0; t < H; t += 2) {
-    const G4Step s2 = info(mA);
-    mA = load_meta(t + 4);
-    step(t, s0, s2, cA, sA);
-    if (t + 1 >= H) break;
-    const G4Step s3 = info(mB);
-    mB = load_meta(t + 5);
-    step(t + 1, s1, s3, cB, sB);
-    s0 = s2;
-    s1 = s3;
-  }
-}
-
-static void launch_wave(const SgmArgs& a, bool up, int n_sv, cudaStream_t st) {
-  dim3 grid((wave_strips(a.W) + WAVE_WARPS - 1) / WAVE_WARPS, n_sv);
-  if (up) k_sgm_wave<true><<<grid, WAVE_WARPS * 32, 0, st>>>(a);
-  else k_sgm_wave<false><<<grid, WAVE_WARPS * 32, 0, st>>>(a);
-}
-
 // u16 aggregation with the per-(seq, view) regime choice: views with reduced
 // intervals run the narrow variant on st_lo[p], wide ones the wide variant on
 // st_hi[p]; each (seq, view) is handled by exactly one of them, so the two
@@ -1118,29 +859,6 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
       hi.S = S[j.part];
       launch_grp4_g(4 << widen, lo, j.fam, j.init, n_sv, st_lo[j.part], j.sweeps);
       launch_grp4_g(8 << widen, hi, j.fam, j.init, n_sv, st_hi[j.part], j.sweeps);
-    }
-    return;
-  }
-  if (g4 && parts == 2 && a.wave_ring[0] && a.wave_ring[1] && true) {
-    // wavefront schedule: S0 = rows ->, columns down + (+1,+1) diagonal
-    // (one wavefront pass), x+y diagonal ->; S1 = rows <-, columns up +
-    // (-1,-1) diagonal, x+y diagonal <-
-    struct Job { int part, fam, sweeps, init; };   // fam < 0: wavefront pass (-1 down, -2 up)
-    const Job jobs[6] = {{0, FAM_H, 1, 1}, {1, FAM_H, 2, 1}, {0, -1, 0, 0},
-                         {1, -2, 0, 0}, {0, FAM_D2, 1, 0}, {1, FAM_D2, 2, 0}};
-    for (const Job& j : jobs) {
-      SgmArgs lo = a, hi = a;
-      lo.select = 1;
-      hi.select = 2;
-      lo.S = S[j.part];
-      hi.S = S[j.part];
-      if (j.fam < 0) {
-        launch_wave(lo, j.fam == -2, n_sv, st_lo[j.part]);
-        launch_wave(hi, j.fam == -2, n_sv, st_hi[j.part]);
-      } else {
-        launch_grp4_g(4 << widen, lo, j.fam, j.init, n_sv, st_lo[j.part], j.sweeps);
-        launch_grp4_g(8 << widen, hi, j.fam, j.init, n_sv, st_hi[j.part], j.sweeps);
-      }
     }
     return;
   }

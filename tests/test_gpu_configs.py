@@ -192,3 +192,57 @@ def test_degenerate_shapes_match_oracle(w, h, d_max):
     frames[1][1] = np.roll(frames[1][0], -1, axis=1)   # some structure to match
     motions = [None, core.make_motion(t=(0.01, 0.0, -0.02))]
     _compare(rig, frames, motions)
+
+
+@pytest.mark.parametrize("window,p1,p2,tau_sad", [(5, 7.0, 86.0, 900.0), (7, 7.0, 86.0, 3000.0),
+                                                  (9, 10.0, 120.0, 5000.0), (3, 1.0, 1.0, 200.0)])
+def test_window_and_penalty_variants_match_oracle(window, p1, p2, tau_sad):
+    """Parameter edges of sgm.py:40-46: window 5 (u16 aggregation), window 7
+    and 9 (the u16 sum bound fails: float32 aggregation, generic cost
+    kernel), P1 == P2 (neighbour terms tie with the m + P2 term), three
+    frames of a rendered scene vs the oracle."""
+    from paper_1708_06301_b200 import core, pipeline, scenes, sgm
+    rig = core.StereoRig(f=160.0, b=0.54, cx=79.5, cy=31.5, width=160, height=64, d_max=47)
+    boxes, poses, motions = scenes.sequence_spec(seed=77 + window, n_frames=3, step=0.5,
+                                                 yaw_deg=0.5, z_range=(2.5, 12.0))
+    frames = _render(rig, [boxes] * 3, poses, seed=9, scale=0.05)
+    params = pipeline.PipelineParams(sgm=sgm.SgmParams(window=window, p1=p1, p2=p2,
+                                                       tau_sad=tau_sad))
+    _compare_params(rig, frames, motions, params,
+                    O.OracleParams(window=window, p1=p1, p2=p2, tau_sad=tau_sad))
+
+
+@pytest.mark.parametrize("w,h,d_max", [(352, 24, 300), (520, 16, 511)])
+def test_large_disparity_range_matches_oracle(w, h, d_max):
+    """d_max beyond config 4's 255 up to the device limit 511 (the widest
+    lane-group instances of the aggregation and WTA): full range then a
+    predicted frame vs the oracle."""
+    from paper_1708_06301_b200 import core
+    rig = core.StereoRig(f=float(w), b=0.5, cx=(w - 1) / 2.0, cy=(h - 1) / 2.0,
+                         width=w, height=h, d_max=d_max)
+    rng = np.random.default_rng(d_max)
+    base = rng.integers(0, 256, (h, w + d_max)).astype(np.uint8)
+    shift = d_max // 3
+    frames = [np.stack([base[:, shift:shift + w], base[:, :w]]) for _ in range(2)]
+    motions = [None, core.make_motion(t=(0.0, 0.0, -0.05))]
+    _compare(rig, frames, motions)
+
+
+def _compare_params(rig, frames, motions, params, oparams):
+    from paper_1708_06301_b200 import core, pipeline
+    pipe = pipeline.DisparityPipeline(rig, params)
+    orc = O.OracleStereo(rig.f, rig.b, rig.cx, rig.cy, rig.width, rig.height, rig.d_max, oparams)
+    for k, (img, motion) in enumerate(zip(frames, motions)):
+        res = pipe.process_frame(core.GrayImage(img[0]), core.GrayImage(img[1]), motion)
+        want = orc.step(img[0], img[1], motion, keep_volumes=True)
+        for view, name in ((0, "left"), (1, "right")):
+            assert np.array_equal(res.total_volume(view), want[name + "_total"]), (k, name)
+            meas = res.measured_left if view == 0 else res.measured_right
+            var = res.measured_left_var if view == 0 else res.measured_right_var
+            assert np.array_equal(meas.values, want[name + "_meas"][0]), (k, name, "wta")
+            assert np.array_equal(var.values, want[name + "_meas"][1]), (k, name, "r")
+            keep = res.keep_left if view == 0 else res.keep_right
+            assert np.array_equal(keep, want[name + "_keep"]), (k, name, "keep")
+            fd = res.fused.left if view == 0 else res.fused.right
+            assert np.array_equal(fd.valid, want[name + "_fused"][2]), (k, name)
+            np.testing.assert_allclose(fd.values, want[name + "_fused"][0], rtol=1e-9, atol=0)

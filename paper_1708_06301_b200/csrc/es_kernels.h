@@ -81,6 +81,11 @@ void launch_aggregate(const SgmArgs& a, int arith, int n_sv, cudaStream_t st);
 // st_lo[p], wide ones on st_hi[p]; all streams may run concurrently
 void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S,
                             const cudaStream_t* st_lo, const cudaStream_t* st_hi);
+// fused column + diagonal pass (es_sgm_vd.cu): the three directions of one
+// row sweep (up = 0: dy = +1, up = 1: dy = -1) in one cluster per view,
+// read-modify-writing the u16 partial sum a.S
+bool vd_supported(int W, int d_max);
+void launch_vd(const SgmArgs& a, bool up, int n_sv, cudaStream_t st);
 
 struct WtaArgs {
   int W, H;

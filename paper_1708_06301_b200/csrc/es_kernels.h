@@ -83,9 +83,9 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
                             const cudaStream_t* st_lo, const cudaStream_t* st_hi);
 // fused column + diagonal pass (es_sgm_vd.cu): the three directions of one
 // row sweep (up = 0: dy = +1, up = 1: dy = -1) in one cluster per view,
-// read-modify-writing the u16 partial sum a.S
+// read-modify-writing (init: writing) the u16 partial sum a.S
 bool vd_supported(int W, int d_max);
-void launch_vd(const SgmArgs& a, bool up, int n_sv, cudaStream_t st);
+void launch_vd(const SgmArgs& a, bool up, bool init, int n_sv, cudaStream_t st);
 
 struct WtaArgs {
   int W, H;

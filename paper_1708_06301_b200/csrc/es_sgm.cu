@@ -865,17 +865,26 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
   static const int vd_env = getenv("ES_SGM_VD") ? atoi(getenv("ES_SGM_VD")) : 0;
   if (g4 && parts == 2 && vd_env && vd_supported(a.W, a.d_max)) {
     // fused column + diagonal passes: S0 = rows ->, then the three dy = +1
-    // directions; S1 = rows <-, then the three dy = -1 directions
+    // directions; S1 = the three dy = -1 directions, then rows <-.  The
+    // cluster passes leave SMs idle (whole 8-SM clusters per GPC); each runs
+    // beside the other stream's row job.
     for (int p = 0; p < 2; ++p) {
       SgmArgs lo = a, hi = a;
       lo.select = 1;
       hi.select = 2;
       lo.S = S[p];
       hi.S = S[p];
-      launch_grp4_g(4 << widen, lo, FAM_H, 1, n_sv, st_lo[p], p ? 2 : 1);
-      launch_grp4_g(8 << widen, hi, FAM_H, 1, n_sv, st_hi[p], p ? 2 : 1);
-      launch_vd(lo, p == 1, n_sv, st_lo[p]);
-      launch_vd(hi, p == 1, n_sv, st_hi[p]);
+      if (p == 0) {
+        launch_grp4_g(4 << widen, lo, FAM_H, 1, n_sv, st_lo[p], 1);
+        launch_grp4_g(8 << widen, hi, FAM_H, 1, n_sv, st_hi[p], 1);
+        launch_vd(lo, false, false, n_sv, st_lo[p]);
+        launch_vd(hi, false, false, n_sv, st_hi[p]);
+      } else {
+        launch_vd(lo, true, true, n_sv, st_lo[p]);
+        launch_vd(hi, true, true, n_sv, st_hi[p]);
+        launch_grp4_g(4 << widen, lo, FAM_H, 0, n_sv, st_lo[p], 2);
+        launch_grp4_g(8 << widen, hi, FAM_H, 0, n_sv, st_hi[p], 2);
+      }
     }
     return;
   }

@@ -14,8 +14,8 @@
 // searched cell the pass reads the cost once and read-modify-writes the
 // partial sum once for three directions (k_sgm_grp4 does both per direction).
 //
-// Work inside a CTA: a warp takes groups of 4 adjacent columns (8 lanes per
-// column, 4 words per lane per 64-cell chunk); per group it loads every old
+// Work inside a CTA: a warp takes groups of 8 adjacent columns (4 lanes per
+// column, 4 words per lane per 32-cell chunk); per group it loads every old
 // state word it needs (own words and the d-1 / d+1 edge words of the three
 // predecessor columns), then computes and stores, so the in-place A state is
 // never read after it is overwritten.  Arithmetic, +inf convention and the
@@ -29,14 +29,15 @@ namespace es {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int VG = 8;                 // lanes per column
+constexpr int VG = 4;                 // lanes per column
 constexpr int VPPL = 4;               // words (u16 pairs) per lane per chunk
-constexpr int VCW = VG * VPPL;        // words per chunk (64 cells)
-constexpr int VNCH = 2;               // chunks per column: d_max <= 127
+constexpr int VCW = VG * VPPL;        // words per chunk (32 cells)
+constexpr int VNCH = 4;               // chunks per column: d_max <= 127
 constexpr int VNW = VCW * VNCH;       // state words per column
 constexpr int VNG = 32 / VG;          // columns per warp group
 constexpr int VC = 8;                 // CTAs per cluster (one cluster per view)
-constexpr int VWARPS = 16;
+constexpr int VGPW = 2;               // column groups per warp (static, every row)
+constexpr int VMAXW = 10;             // warps per CTA at most: 20 groups = 160 columns
 constexpr int VSLOT = 5 * VNW + 10;   // smem words per column slot (A, 2 B, 2 C, 5 m pairs)
 
 __host__ __device__ inline void vd_range(int W, int k, int& c0, int& nc) {
@@ -90,8 +91,15 @@ __device__ __forceinline__ void vd_path(const uint32_t (&P)[VPPL], uint32_t el, 
   }
 }
 
-template <bool UP>
-__global__ void __cluster_dims__(VC, 1, 1) __launch_bounds__(VWARPS * 32, 1) k_sgm_vd(SgmArgs a) {
+// operands of one (group, row) work item, loaded one item ahead
+struct VdOps {
+  uint2 mt;
+  uint32_t cn[VNCH][VPPL];
+  uint32_t sn[VNCH][VPPL];
+};
+
+template <bool UP, bool INIT>
+__global__ void __cluster_dims__(VC, 1, 1) __launch_bounds__(VMAXW * 32, 1) k_sgm_vd(SgmArgs a) {
   extern __shared__ __align__(16) uint32_t vsm[];
   const int W = a.W, H = a.H;
   if (a.select) {   // uniform over the cluster (one view)
@@ -102,12 +110,14 @@ __global__ void __cluster_dims__(VC, 1, 1) __launch_bounds__(VWARPS * 32, 1) k_s
   int c0, nc;
   vd_range(W, k, c0, nc);
   const int NS = vd_maxcols(W) + 2;   // column slots: halo, owned columns, halo
-  uint32_t* SA = vsm;                 // [NS][VNW]        column path (in place)
-  uint32_t* SB = SA + NS * VNW;       // [2][NS][VNW]     predecessor x-1
-  uint32_t* SC = SB + 2 * NS * VNW;   // [2][NS][VNW]     predecessor x+1
+  uint32_t* SA = vsm;                 // [VNCH][NS][VCW]     column path (in place)
+  uint32_t* SB = SA + NS * VNW;       // [2][VNCH][NS][VCW]  predecessor x-1
+  uint32_t* SC = SB + 2 * NS * VNW;   // [2][VNCH][NS][VCW]  predecessor x+1
   uint32_t* MA = SC + 2 * NS * VNW;   // [NS][2]          (m + P2, -m) splats
   uint32_t* MB = MA + 2 * NS;         // [2][NS][2]
   uint32_t* MC = MB + 4 * NS;         // [2][NS][2]
+  const int CS = NS * VCW;            // chunk stride of a state buffer (words)
+  const int PS = VNCH * CS;           // parity stride of the B / C buffers
   for (int i = threadIdx.x; i < NS * VSLOT; i += blockDim.x) vsm[i] = INF16x2;
   // halo slots: CTA k-1 writes this CTA's left halo (slot 0), CTA k+1 the
   // right one (slot nc + 1); off-image halos keep the +inf / no-m init
@@ -121,21 +131,64 @@ __global__ void __cluster_dims__(VC, 1, 1) __launch_bounds__(VWARPS * 32, 1) k_s
   uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
   const uint32_t p1x2 = a.p1i * 0x10001u;
   const int ngroups = nc / VNG;
-  int ncl = 0, ncr = 0, tmp;
+  // a warp owns VGPW consecutive column groups, the same in every row
+  const int g_first = warp * VGPW;
+  const int g_end = min(g_first + VGPW, ngroups);
+  const int n_items = g_end > g_first ? g_end - g_first : 0;
+  int ncl = 0, tmp;
   if (k > 0) vd_range(W, k - 1, tmp, ncl);
-  if (k + 1 < VC) vd_range(W, k + 1, tmp, ncr);
-  (void)ncl;
 
+  // work items: (row t, group i) in sweep order; metadata is loaded two
+  // items ahead, cost and partial-sum words one item ahead
+  auto load_meta = [&](int item) -> uint2 {
+    uint2 m = make_uint2(0xFFFFFFFFu, 0u);
+    if (n_items == 0) return m;
+    const int t = item / n_items, g = g_first + item % n_items;
+    const int x = c0 + g * VNG + q;
+    if (t < H && x < W) m = meta[(size_t)(UP ? H - 1 - t : t) * W + x];
+    return m;
+  };
+  auto fetch = [&](uint2 mt, VdOps& o) {
+    o.mt = mt;
+    int base = 0, relb = 0;
+    uint32_t spanp = 0u;
+    if (mt.x != 0xFFFFFFFFu) {
+      const int j0 = (int)((mt.x & 0xFFFFu) >> 1), j1 = (int)((mt.x >> 16) >> 1);
+      base = (int)(mt.y - (uint32_t)j0) + VPPL * gl;
+      relb = VPPL * gl - j0 + VPPL - 1;
+      spanp = (uint32_t)(j1 - j0 + VPPL);
+    }
+#pragma unroll
+    for (int c = 0; c < VNCH; ++c) {
+      const bool p = (uint32_t)(relb + c * VCW) < spanp;
+      uint32_t v0 = INF16x2, v1 = INF16x2, v2 = INF16x2, v3 = INF16x2;
+      asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}\n"
+                   : "+r"(v0), "+r"(v1), "+r"(v2), "+r"(v3) : "l"(C + base + c * VCW), "r"((int)p));
+      o.cn[c][0] = v0; o.cn[c][1] = v1; o.cn[c][2] = v2; o.cn[c][3] = v3;
+      uint32_t s0 = 0u, s1 = 0u, s2 = 0u, s3 = 0u;
+      if constexpr (!INIT) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}\n"
+                     : "=r"(s0), "=r"(s1), "=r"(s2), "=r"(s3) : "l"(S + base + c * VCW), "r"((int)p));
+      }
+      o.sn[c][0] = s0; o.sn[c][1] = s1; o.sn[c][2] = s2; o.sn[c][3] = s3;
+    }
+  };
+
+  VdOps cur, nxt;
+  fetch(load_meta(0), cur);
+  uint2 m1 = load_meta(1);
+  const int total = n_items * H;
+  int item = 0;
   for (int t = 0; t < H; ++t) {
-    const int y = UP ? H - 1 - t : t;
     const int nw = t & 1, ow = nw ^ 1;
-    for (int g = warp; g < ngroups; g += VWARPS) {
+    for (int i = 0; i < n_items; ++i, ++item) {
+      const uint2 m2 = load_meta(item + 2);
+      if (item + 1 < total) fetch(m1, nxt);   // next group, or the next row's first
+      m1 = m2;
+      const int g = g_first + i;
       const int lc = g * VNG + q;
-      const int x = c0 + lc;
       const int slot = lc + 1;
-      // pixel metadata (grp4 encoding)
-      uint2 mt = make_uint2(0xFFFFFFFFu, 0u);
-      if (x < W) mt = meta[(size_t)y * W + x];
+      const uint2 mt = cur.mt;
       int base = 0, relb = 0, clo = VNCH, chi = -1;
       uint32_t spanp = 0u;
       if (mt.x != 0xFFFFFFFFu) {
@@ -147,75 +200,62 @@ __global__ void __cluster_dims__(VC, 1, 1) __launch_bounds__(VWARPS * 32, 1) k_s
         chi = j1 / VCW;
       }
       const int ulo = __reduce_min_sync(FULL, clo), uhi = __reduce_max_sync(FULL, chi);
-      // ---- load phase: every old word this group needs
-      uint32_t PA[VNCH][VPPL], PB[VNCH][VPPL], PC[VNCH][VPPL];
-      uint32_t eA[VNCH][2], eB[VNCH][2], eC[VNCH][2];
-      uint32_t cn[VNCH][VPPL], sn[VNCH][VPPL];
-      const uint32_t* a_col = SA + slot * VNW;
-      const uint32_t* b_col = SB + (ow * NS + slot - 1) * VNW;
-      const uint32_t* c_col = SC + (ow * NS + slot + 1) * VNW;
+      // state layout [parity][chunk][slot][VCW words]: a warp's 8 columns of
+      // one chunk are 512 contiguous bytes (conflict-free 16-byte accesses)
+      const uint32_t* a_col = SA + slot * VCW;
+      const uint32_t* b_col = SB + ow * PS + (slot - 1) * VCW;
+      const uint32_t* c_col = SC + ow * PS + (slot + 1) * VCW;
+      // d-1 / d+1 edge words of every chunk, before any in-place store
+      uint32_t e[VNCH][6];
 #pragma unroll
       for (int c = 0; c < VNCH; ++c) {
-        if (c < ulo || c > uhi) continue;
-        const int w0 = c * VCW + gl * VPPL;
-        const bool p = (uint32_t)(relb + c * VCW) < spanp;
-        {
-          const uint32_t* src = p ? C + base + c * VCW : nullptr;
-          uint32_t v0 = INF16x2, v1 = INF16x2, v2 = INF16x2, v3 = INF16x2;
-          if (p) {
-            asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3) : "l"(src));
-          }
-          cn[c][0] = v0; cn[c][1] = v1; cn[c][2] = v2; cn[c][3] = v3;
-          uint32_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-          if (p) {
-            asm volatile("ld.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(s0), "=r"(s1), "=r"(s2), "=r"(s3) : "l"(S + base + c * VCW));
-          }
-          sn[c][0] = s0; sn[c][1] = s1; sn[c][2] = s2; sn[c][3] = s3;
-        }
-        const uint4 va = lds4(a_col + w0), vb = lds4(b_col + w0), vc = lds4(c_col + w0);
-        PA[c][0] = va.x; PA[c][1] = va.y; PA[c][2] = va.z; PA[c][3] = va.w;
-        PB[c][0] = vb.x; PB[c][1] = vb.y; PB[c][2] = vb.z; PB[c][3] = vb.w;
-        PC[c][0] = vc.x; PC[c][1] = vc.y; PC[c][2] = vc.z; PC[c][3] = vc.w;
-        const bool hasl = w0 > 0, hasr = w0 + VPPL < VNW;
-        eA[c][0] = hasl ? a_col[w0 - 1] : INF16x2;
-        eB[c][0] = hasl ? b_col[w0 - 1] : INF16x2;
-        eC[c][0] = hasl ? c_col[w0 - 1] : INF16x2;
-        eA[c][1] = hasr ? a_col[w0 + VPPL] : INF16x2;
-        eB[c][1] = hasr ? b_col[w0 + VPPL] : INF16x2;
-        eC[c][1] = hasr ? c_col[w0 + VPPL] : INF16x2;
+        const int w0 = gl * VPPL;
+        // d-1 of the lane's first word: the previous lane's last word, or the
+        // previous chunk's last word; d+1 of its last word likewise
+        const int wl = gl > 0 ? c * CS + w0 - 1 : (c > 0 ? (c - 1) * CS + VCW - 1 : 0);
+        const int wr = gl < VG - 1 ? c * CS + w0 + VPPL : (c + 1 < VNCH ? (c + 1) * CS : 0);
+        e[c][0] = a_col[wl]; e[c][1] = a_col[wr];
+        e[c][2] = b_col[wl]; e[c][3] = b_col[wr];
+        e[c][4] = c_col[wl]; e[c][5] = c_col[wr];
+        if (gl == 0 && c == 0) e[c][0] = e[c][2] = e[c][4] = INF16x2;
+        if (gl == VG - 1 && c + 1 == VNCH) e[c][1] = e[c][3] = e[c][5] = INF16x2;
       }
       const uint2 mA = *reinterpret_cast<const uint2*>(MA + 2 * slot);
       const uint2 mB = *reinterpret_cast<const uint2*>(MB + 2 * (ow * NS + slot - 1));
       const uint2 mC = *reinterpret_cast<const uint2*>(MC + 2 * (ow * NS + slot + 1));
       __syncwarp();
-      // ---- compute and store phase
-      uint32_t* a_out = SA + slot * VNW;
-      uint32_t* b_out = SB + (nw * NS + slot) * VNW;
-      uint32_t* c_out = SC + (nw * NS + slot) * VNW;
+      uint32_t* a_out = SA + slot * VCW;
+      uint32_t* b_out = SB + nw * PS + slot * VCW;
+      uint32_t* c_out = SC + nw * PS + slot * VCW;
       uint32_t nA = INF16x2, nB = INF16x2, nC = INF16x2;
 #pragma unroll
       for (int c = 0; c < VNCH; ++c) {
-        const int w0 = c * VCW + gl * VPPL;
+        const int w0 = c * CS + gl * VPPL;
         if (c < ulo || c > uhi) {
           sts4(a_out + w0, INF16x2, INF16x2, INF16x2, INF16x2);
           sts4(b_out + w0, INF16x2, INF16x2, INF16x2, INF16x2);
           sts4(c_out + w0, INF16x2, INF16x2, INF16x2, INF16x2);
           continue;
         }
-        uint32_t LA[VPPL], LB[VPPL], LC[VPPL], Ss[VPPL];
-        vd_path(PA[c], eA[c][0], eA[c][1], mA.x, mA.y, p1x2, cn[c], LA);
-        vd_path(PB[c], eB[c][0], eB[c][1], mB.x, mB.y, p1x2, cn[c], LB);
-        vd_path(PC[c], eC[c][0], eC[c][1], mC.x, mC.y, p1x2, cn[c], LC);
+        uint32_t P[VPPL], LA[VPPL], LB[VPPL], LC[VPPL], Ss[VPPL];
+        uint4 v = lds4(a_col + w0);
+        P[0] = v.x; P[1] = v.y; P[2] = v.z; P[3] = v.w;
+        vd_path(P, e[c][0], e[c][1], mA.x, mA.y, p1x2, cur.cn[c], LA);
+        v = lds4(b_col + w0);
+        P[0] = v.x; P[1] = v.y; P[2] = v.z; P[3] = v.w;
+        vd_path(P, e[c][2], e[c][3], mB.x, mB.y, p1x2, cur.cn[c], LB);
+        v = lds4(c_col + w0);
+        P[0] = v.x; P[1] = v.y; P[2] = v.z; P[3] = v.w;
+        vd_path(P, e[c][4], e[c][5], mC.x, mC.y, p1x2, cur.cn[c], LC);
 #pragma unroll
-        for (int i = 0; i < VPPL; ++i) Ss[i] = __vadd2(sn[c][i], __vadd2(LA[i], __vadd2(LB[i], LC[i])));
-        const bool p = (uint32_t)(relb + c * VCW) < spanp;
-        if (p) {
-          asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};"
-                       :: "l"(S + base + c * VCW), "r"(Ss[0]), "r"(Ss[1]), "r"(Ss[2]), "r"(Ss[3])
-                       : "memory");
+        for (int r = 0; r < VPPL; ++r) {
+          Ss[r] = __vadd2(LA[r], __vadd2(LB[r], LC[r]));
+          if constexpr (!INIT) Ss[r] = __vadd2(cur.sn[c][r], Ss[r]);
         }
+        const bool p = (uint32_t)(relb + c * VCW) < spanp;
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.global.v4.u32 [%0], {%1, %2, %3, %4};\n\t}\n"
+                     :: "l"(S + base + c * VCW), "r"(Ss[0]), "r"(Ss[1]), "r"(Ss[2]), "r"(Ss[3]), "r"((int)p)
+                     : "memory");
         sts4(a_out + w0, LA[0], LA[1], LA[2], LA[3]);
         sts4(b_out + w0, LB[0], LB[1], LB[2], LB[3]);
         sts4(c_out + w0, LC[0], LC[1], LC[2], LC[3]);
@@ -250,24 +290,24 @@ __global__ void __cluster_dims__(VC, 1, 1) __launch_bounds__(VWARPS * 32, 1) k_s
         const int hs = ncl + 1;
 #pragma unroll
         for (int c = 0; c < VNCH; ++c) {
-          const int w0 = c * VCW + gl * VPPL;
-          st_cluster4(SC + (nw * NS + hs) * VNW + w0, k - 1, lds4(c_out + w0));
+          const int w0 = c * CS + gl * VPPL;
+          st_cluster4(SC + nw * PS + hs * VCW + w0, k - 1, lds4(c_out + w0));
         }
         if (gl == 0) st_cluster2(MC + 2 * (nw * NS + hs), k - 1, mc, ncv);
       }
       if (lc == nc - 1 && k + 1 < VC) {
 #pragma unroll
         for (int c = 0; c < VNCH; ++c) {
-          const int w0 = c * VCW + gl * VPPL;
-          st_cluster4(SB + (nw * NS + 0) * VNW + w0, k + 1, lds4(b_out + w0));
+          const int w0 = c * CS + gl * VPPL;
+          st_cluster4(SB + nw * PS + w0, k + 1, lds4(b_out + w0));
         }
         if (gl == 0) st_cluster2(MB + 2 * (nw * NS + 0), k + 1, mb, nb);
       }
       __syncwarp();
+      cur = nxt;
     }
     cluster_sync_all();
   }
-  (void)ncr;
 }
 
 }  // namespace
@@ -275,25 +315,29 @@ __global__ void __cluster_dims__(VC, 1, 1) __launch_bounds__(VWARPS * 32, 1) k_s
 bool vd_supported(int W, int d_max) {
   static int ok = -1;
   if (npairs_max(d_max) > VNW || W < VC * VNG) return false;
+  if (vd_maxcols(W) / VNG > VMAXW * VGPW) return false;
   const size_t smem = vd_smem_bytes(W);
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (smem > (size_t)optin) return false;
   if (ok < 0) {
-    ok = cudaFuncSetAttribute(k_sgm_vd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
-                 cudaSuccess &&
-         cudaFuncSetAttribute(k_sgm_vd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
-                 cudaSuccess;
+    ok = 1;
+    for (auto k : {k_sgm_vd<false, false>, k_sgm_vd<true, false>, k_sgm_vd<false, true>,
+                   k_sgm_vd<true, true>})
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        ok = 0;
   }
   return ok == 1;
 }
 
-void launch_vd(const SgmArgs& a, bool up, int n_sv, cudaStream_t st) {
+void launch_vd(const SgmArgs& a, bool up, bool init, int n_sv, cudaStream_t st) {
   const size_t smem = vd_smem_bytes(a.W);
-  auto k = up ? k_sgm_vd<true> : k_sgm_vd<false>;
+  auto k = up ? (init ? k_sgm_vd<true, true> : k_sgm_vd<true, false>)
+              : (init ? k_sgm_vd<false, true> : k_sgm_vd<false, false>);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k<<<dim3(VC, n_sv), VWARPS * 32, smem, st>>>(a);
+  const int nwarps = (vd_maxcols(a.W) / VNG + VGPW - 1) / VGPW;
+  k<<<dim3(VC, n_sv), nwarps * 32, smem, st>>>(a);
 }
 
 }  // namespace es

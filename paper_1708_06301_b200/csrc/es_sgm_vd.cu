@@ -35,9 +35,9 @@ constexpr int VCW = VG * VPPL;        // words per chunk (32 cells)
 constexpr int VNCH = 4;               // chunks per column: d_max <= 127
 constexpr int VNW = VCW * VNCH;       // state words per column
 constexpr int VNG = 32 / VG;          // columns per warp group
-constexpr int VC = 8;                 // CTAs per cluster (one cluster per view)
+constexpr int VC = 9;                 // CTAs per cluster (one cluster per view; 9 x 1-CTA SMs pack 15 clusters = 135 SMs)
 constexpr int VGPW = 2;               // column groups per warp (static, every row)
-constexpr int VMAXW = 10;             // warps per CTA at most: 20 groups = 160 columns
+constexpr int VMAXW = 10;             // warps per CTA at most: 20 groups = 160 columns per CTA
 constexpr int VSLOT = 5 * VNW + 10;   // smem words per column slot (A, 2 B, 2 C, 5 m pairs)
 
 __host__ __device__ inline void vd_range(int W, int k, int& c0, int& nc) {
@@ -50,7 +50,10 @@ __host__ __device__ inline int vd_maxcols(int W) {
   const int ng = (W + VNG - 1) / VNG;
   return ((ng + VC - 1) / VC) * VNG;
 }
-inline size_t vd_smem_bytes(int W) { return sizeof(uint32_t) * (size_t)(vd_maxcols(W) + 2) * VSLOT; }
+// state slots plus four halo mbarriers (left / right x row parity)
+inline size_t vd_smem_bytes(int W) {
+  return sizeof(uint32_t) * (size_t)(vd_maxcols(W) + 2) * VSLOT + 32 + sizeof(int) * VMAXW;
+}
 
 __device__ __forceinline__ uint4 lds4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
 __device__ __forceinline__ void sts4(uint32_t* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -70,6 +73,21 @@ __device__ __forceinline__ void st_cluster2(const uint32_t* local, int rank, uin
   unsigned ra;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(rank));
   asm volatile("st.shared::cluster.v2.u32 [%0], {%1, %2};" :: "r"(ra), "r"(x), "r"(y) : "memory");
+}
+// remote arrive (release at cluster scope) on the same mbarrier of CTA `rank`
+__device__ __forceinline__ void mbar_arrive_remote(const uint64_t* local, int rank) {
+  const unsigned la = (unsigned)__cvta_generic_to_shared(local);
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(ra) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(const uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}\n"
+                 : "=r"(done) : "r"(a), "r"(parity) : "memory");
 }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -118,9 +136,20 @@ __global__ void __cluster_dims__(VC, 1, 1) __launch_bounds__(VMAXW * 32, 1) k_sg
   uint32_t* MC = MB + 4 * NS;         // [2][NS][2]
   const int CS = NS * VCW;            // chunk stride of a state buffer (words)
   const int PS = VNCH * CS;           // parity stride of the B / C buffers
+  uint64_t* hbar = reinterpret_cast<uint64_t*>(vsm + NS * VSLOT);   // [L0, L1, R0, R1]
+  volatile int* done = reinterpret_cast<volatile int*>(hbar + 4);   // [warp]: rows completed
   for (int i = threadIdx.x; i < NS * VSLOT; i += blockDim.x) vsm[i] = INF16x2;
+  if (threadIdx.x < VMAXW) done[threadIdx.x] = 0;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 4; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;"
+                   :: "r"((unsigned)__cvta_generic_to_shared(hbar + b)), "r"(VG) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   // halo slots: CTA k-1 writes this CTA's left halo (slot 0), CTA k+1 the
-  // right one (slot nc + 1); off-image halos keep the +inf / no-m init
+  // right one (slot nc + 1), each followed by one arrive per writing lane on
+  // this CTA's left / right mbarrier of that row's parity; off-image halos
+  // keep the +inf / no-m init
   cluster_sync_all();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -179,8 +208,27 @@ __global__ void __cluster_dims__(VC, 1, 1) __launch_bounds__(VMAXW * 32, 1) k_sg
   uint2 m1 = load_meta(1);
   const int total = n_items * H;
   int item = 0;
+  const bool reads_left = g_first == 0 && n_items > 0 && k > 0;
+  const bool reads_right = n_items > 0 && g_end == ngroups && k + 1 < VC;
   for (int t = 0; t < H; ++t) {
     const int nw = t & 1, ow = nw ^ 1;
+    if (t > 0) {
+      // the neighbouring warps' columns of row t-1 (this CTA): both have
+      // finished row t-1, so its state is complete and they no longer read
+      // the buffers row t overwrites
+      if (lane == 0) {
+        const int nwarps = blockDim.x >> 5;
+        if (warp > 0) while (done[warp - 1] < t) { }
+        if (warp + 1 < nwarps) while (done[warp + 1] < t) { }
+        __threadfence_block();
+      }
+      __syncwarp();
+      // the neighbouring CTAs' edge columns of row t-1 (a barrier per
+      // parity: a neighbour is never two pushes ahead on the same one)
+      const unsigned ph = (unsigned)(((t - 1) >> 1) & 1);
+      if (reads_left) mbar_wait(hbar + ((t - 1) & 1), ph);
+      if (reads_right) mbar_wait(hbar + 2 + ((t - 1) & 1), ph);
+    }
     for (int i = 0; i < n_items; ++i, ++item) {
       const uint2 m2 = load_meta(item + 2);
       if (item + 1 < total) fetch(m1, nxt);   // next group, or the next row's first
@@ -294,6 +342,7 @@ __global__ void __cluster_dims__(VC, 1, 1) __launch_bounds__(VMAXW * 32, 1) k_sg
           st_cluster4(SC + nw * PS + hs * VCW + w0, k - 1, lds4(c_out + w0));
         }
         if (gl == 0) st_cluster2(MC + 2 * (nw * NS + hs), k - 1, mc, ncv);
+        mbar_arrive_remote(hbar + 2 + nw, k - 1);   // CTA k-1's right mbarrier
       }
       if (lc == nc - 1 && k + 1 < VC) {
 #pragma unroll
@@ -302,12 +351,18 @@ __global__ void __cluster_dims__(VC, 1, 1) __launch_bounds__(VMAXW * 32, 1) k_sg
           st_cluster4(SB + nw * PS + w0, k + 1, lds4(b_out + w0));
         }
         if (gl == 0) st_cluster2(MB + 2 * (nw * NS + 0), k + 1, mb, nb);
+        mbar_arrive_remote(hbar + nw, k + 1);       // CTA k+1's left mbarrier
       }
       __syncwarp();
       cur = nxt;
     }
-    cluster_sync_all();
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      done[warp] = t + 1;
+    }
   }
+  cluster_sync_all();   // no CTA leaves while a neighbour may still push into it
 }
 
 }  // namespace
@@ -325,7 +380,8 @@ bool vd_supported(int W, int d_max) {
     ok = 1;
     for (auto k : {k_sgm_vd<false, false>, k_sgm_vd<true, false>, k_sgm_vd<false, true>,
                    k_sgm_vd<true, true>})
-      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         ok = 0;
   }
   return ok == 1;
@@ -335,6 +391,7 @@ void launch_vd(const SgmArgs& a, bool up, bool init, int n_sv, cudaStream_t st) 
   const size_t smem = vd_smem_bytes(a.W);
   auto k = up ? (init ? k_sgm_vd<true, true> : k_sgm_vd<true, false>)
               : (init ? k_sgm_vd<false, true> : k_sgm_vd<false, false>);
+  cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nwarps = (vd_maxcols(a.W) / VNG + VGPW - 1) / VGPW;
   k<<<dim3(VC, n_sv), nwarps * 32, smem, st>>>(a);

@@ -879,6 +879,13 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
         launch_grp4_g(8 << widen, hi, FAM_H, 1, n_sv, st_hi[p], 1);
         launch_vd(lo, false, false, n_sv, st_lo[p]);
         launch_vd(hi, false, false, n_sv, st_hi[p]);
+      } else if (vd_env == 2) {
+        // mixed: the dy = -1 directions as grp4 jobs beside the cluster pass
+        const int fam_sw[4][3] = {{FAM_H, 2, 1}, {FAM_V, 2, 0}, {FAM_D1, 2, 0}, {FAM_D2, 2, 0}};
+        for (const auto& j : fam_sw) {
+          launch_grp4_g(4 << widen, lo, j[0], j[2], n_sv, st_lo[p], j[1]);
+          launch_grp4_g(8 << widen, hi, j[0], j[2], n_sv, st_hi[p], j[1]);
+        }
       } else {
         launch_vd(lo, true, true, n_sv, st_lo[p]);
         launch_vd(hi, true, true, n_sv, st_hi[p]);

@@ -49,7 +49,7 @@ hdr = rows[0]
 lines.append(f"## ncu --set full, one timed step (B={batch}), `{tag}`\n")
 lines.append("| kernel | ms | DRAM GB | DRAM % peak | warps active % | issue active % | regs | top stalls (cycles per issue) |")
 lines.append("|---|---|---|---|---|---|---|---|")
-agg_bytes, agg_ms = 0.0, 0.0
+agg_bytes, agg_ms, agg_alu = 0.0, 0.0, 0.0
 table = []
 for r in rows[2:]:
     d = dict(zip(hdr, r))
@@ -62,6 +62,7 @@ for r in rows[2:]:
     if "grp4" in name:
         agg_bytes += dram
         agg_ms += ms
+        agg_alu += ms * float(d["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"])
     st = {k: float(v) for k, v in d.items() if k.startswith("smsp__average_warps_issue_stalled")
           and k.endswith("per_issue_active.ratio") and v}
     top = ", ".join("%s %.1f" % (k.replace("smsp__average_warps_issue_stalled_", "").replace(
@@ -79,6 +80,9 @@ with open(os.path.join(outdir, f"SUMMARY_{tag}.md"), "w") as fh:
     fh.write("\n".join(lines) + "\n")
 json.dump({"batch": batch, "texture_scale": tex, "config": 5, "dram_bytes_per_step": agg_bytes,
            "kernel_ms_per_step_serialised": agg_ms,
+           "alu_pipe_active_pct": agg_alu / agg_ms if agg_ms else None,
+           "alu_source": "time-weighted sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active "
+                         "over the same k_sgm_grp4 launches",
            "source": f"profiles/r01/SUMMARY_{tag}.md: sum of dram__bytes_read.sum + dram__bytes_write.sum "
                      f"over the k_sgm_grp4 launches of one timed step (ncu --set full)"},
           open(os.path.join(outdir, "agg_traffic.json"), "w"), indent=1)

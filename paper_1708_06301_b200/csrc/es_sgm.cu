@@ -11,6 +11,10 @@
 //               (8 cells) of each absolute chunk; see its own comment and
 //               DESIGN.md section 4.  Launched as six jobs per step over two
 //               (or four) partial sums by launch_aggregate_parts.
+//   k_sgm_vd    (u16, opt-in ES_SGM_VD=1 / 2, es_sgm_vd.cu): the three
+//               directions of one row sweep over columns and diagonals in one
+//               thread-block cluster per view; parity-green, not yet faster
+//               than the grp4 jobs (profiles/r01/SUMMARY_vd.md).
 //   k_sgm_grp3  (u16): the previous production kernel, A/B baseline
 //               (ES_SGM_G4=0).
 //   k_sgm       (u16 / f32): one warp per chain, lane l holding pair

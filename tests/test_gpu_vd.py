@@ -28,3 +28,18 @@ def test_fused_cluster_pass_matches(mode, tests):
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:]
+
+
+@pytest.mark.parametrize("mode", ["1", "2"])
+@pytest.mark.parametrize("shape", [(310, 94, 40), (1242, 40, 127), (96, 32, 31)])
+def test_fused_cluster_pass_total_volumes(mode, shape):
+    """The aggregated volumes themselves (not only the winners) of a batch of
+    9 sequences, three of them checked against the oracle, for image widths
+    that leave trailing CTAs of a cluster without columns (310, 96) and the
+    full config width (1242)."""
+    w, h, d = shape
+    env = dict(os.environ, ES_SGM_VD=mode)
+    r = subprocess.run([sys.executable, os.path.join(HERE, "vd_volume_check.py"), str(w), str(h),
+                        str(d), "9", "3"], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=1200)
+    assert r.returncode == 0 and "volumes ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]

@@ -556,7 +556,7 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
       if (p) CK(cudaStreamWaitEvent(lo[p], c->ev_fork, 0));
       CK(cudaStreamWaitEvent(hi[p], c->ev_fork, 0));
     }
-    launch_aggregate_parts(sa, n_sv, P, S, lo, hi);
+    const int live = launch_aggregate_parts(sa, n_sv, P, S, lo, hi);
     for (int p = 0; p < P; ++p) {
       for (cudaStream_t s : {lo[p], hi[p]}) {
         if (s == c->st) continue;
@@ -564,7 +564,7 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
         CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
       }
     }
-    c->parts_live = P;
+    c->parts_live = live;
   } else {
     launch_aggregate(sa, c->arith, n_sv, c->st);
     c->parts_live = 1;

@@ -79,8 +79,9 @@ void launch_aggregate(const SgmArgs& a, int arith, int n_sv, cudaStream_t st);
 // u16 only, a.cells required: the 4 path families accumulate into `parts`
 // (1, 2 or 4) partial sums S[k % parts]; reduced-interval (seq, view)s run on
 // st_lo[p], wide ones on st_hi[p]; all streams may run concurrently
-void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S,
-                            const cudaStream_t* st_lo, const cudaStream_t* st_hi);
+// returns the number of partial sums holding the total (<= parts)
+int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S,
+                           const cudaStream_t* st_lo, const cudaStream_t* st_hi);
 // fused column + diagonal pass (es_sgm_vd.cu): the three directions of one
 // row sweep (up = 0: dy = +1, up = 1: dy = -1) in one cluster per view,
 // read-modify-writing (init: writing) the u16 partial sum a.S

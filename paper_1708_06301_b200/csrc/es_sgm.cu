@@ -831,7 +831,7 @@ static void launch_grp4_g(int G, const SgmArgs& a, int fam, int init, int n_sv, 
 // st_hi[p]; each (seq, view) is handled by exactly one of them, so the two
 // never touch the same volume and run concurrently.  Jobs into the same
 // partial sum are ordered on its stream pair.
-void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S,
+int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S,
                             const cudaStream_t* st_lo, const cudaStream_t* st_hi) {
   // parts partial sums: family k accumulates into S[k % parts] on streams
   // st_lo/st_hi[k % parts]; each (seq, view) uses exactly one of lo / hi
@@ -846,6 +846,32 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
   int widen = widen_env >= 0 ? widen_env : (n_sv <= 2 && np <= 64 ? 1 : 0);
   if (np > 64) widen += 1;
   static const int split_env = getenv("ES_SGM_SPLITH") ? atoi(getenv("ES_SGM_SPLITH")) : 1;
+  static const int vd3_env = getenv("ES_SGM_VD") ? atoi(getenv("ES_SGM_VD")) : 0;
+  if (g4 && parts == 4 && vd3_env == 3 && vd_supported(a.W, a.d_max)) {
+    // three live partial sums: S2 = the cluster pass of the dy = +1
+    // directions (writing, no dependency), concurrent with S0 = rows ->,
+    // columns up, x-y diagonal up and S1 = rows <-, x+y diagonal up
+    SgmArgs lo2 = a, hi2 = a;
+    lo2.select = 1;
+    hi2.select = 2;
+    lo2.S = S[2];
+    hi2.S = S[2];
+    launch_vd(lo2, false, true, n_sv, st_lo[2]);
+    launch_vd(hi2, false, true, n_sv, st_hi[2]);
+    struct Job { int part, fam, sweeps, init; };
+    const Job jobs[5] = {{0, FAM_H, 1, 1}, {1, FAM_H, 2, 1}, {0, FAM_V, 2, 0},
+                         {1, FAM_D2, 2, 0}, {0, FAM_D1, 2, 0}};
+    for (const Job& j : jobs) {
+      SgmArgs lo = a, hi = a;
+      lo.select = 1;
+      hi.select = 2;
+      lo.S = S[j.part];
+      hi.S = S[j.part];
+      launch_grp4_g(4 << widen, lo, j.fam, j.init, n_sv, st_lo[j.part], j.sweeps);
+      launch_grp4_g(8 << widen, hi, j.fam, j.init, n_sv, st_hi[j.part], j.sweeps);
+    }
+    return 3;
+  }
   if (g4 && parts == 4 && split_env) {
     // small batches are latency-bound on the longest chain walk (a row's
     // 2W steps): the row family's two sweeps run as separate jobs into their
@@ -864,7 +890,7 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
       launch_grp4_g(4 << widen, lo, j.fam, j.init, n_sv, st_lo[j.part], j.sweeps);
       launch_grp4_g(8 << widen, hi, j.fam, j.init, n_sv, st_hi[j.part], j.sweeps);
     }
-    return;
+    return parts;
   }
   static const int vd_env = getenv("ES_SGM_VD") ? atoi(getenv("ES_SGM_VD")) : 0;
   if (g4 && parts == 2 && vd_env && vd_supported(a.W, a.d_max)) {
@@ -897,7 +923,7 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
         launch_grp4_g(8 << widen, hi, FAM_H, 0, n_sv, st_hi[p], 2);
       }
     }
-    return;
+    return parts;
   }
   static const int split2_env = getenv("ES_SGM_SPLIT2") ? atoi(getenv("ES_SGM_SPLIT2")) : 1;
   if (g4 && parts == 2 && split2_env) {
@@ -917,7 +943,7 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
       launch_grp4_g(4 << widen, lo, j.fam, j.init, n_sv, st_lo[j.part], j.sweeps);
       launch_grp4_g(8 << widen, hi, j.fam, j.init, n_sv, st_hi[j.part], j.sweeps);
     }
-    return;
+    return parts;
   }
   if (g4) {
     for (int k = 0; k < 4; ++k) {
@@ -931,7 +957,7 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
       launch_grp4_g(4 << widen, lo, fams[k], init, n_sv, st_lo[p]);
       launch_grp4_g(8 << widen, hi, fams[k], init, n_sv, st_hi[p]);
     }
-    return;
+    return parts;
   }
   for (int k = 0; k < 4; ++k) {
     const int p = k % parts;
@@ -957,6 +983,7 @@ void launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* 
       launch_grp3<32>(hi, np, fams[k], 3, init, n_sv, st_hi[p]);
     }
   }
+  return parts;
 }
 
 void launch_aggregate(const SgmArgs& a, int arith, int n_sv, cudaStream_t st) {

@@ -30,7 +30,7 @@ def test_fused_cluster_pass_matches(mode, tests):
     assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:]
 
 
-@pytest.mark.parametrize("mode", ["1", "2"])
+@pytest.mark.parametrize("mode", ["1", "2", "3"])
 @pytest.mark.parametrize("shape", [(310, 94, 40), (1242, 40, 127), (96, 32, 31)])
 def test_fused_cluster_pass_total_volumes(mode, shape):
     """The aggregated volumes themselves (not only the winners) of a batch of
@@ -39,6 +39,8 @@ def test_fused_cluster_pass_total_volumes(mode, shape):
     full config width (1242)."""
     w, h, d = shape
     env = dict(os.environ, ES_SGM_VD=mode)
+    if mode == "3":   # the cluster pass into a third partial sum, concurrent with grp4 jobs
+        env["ES_SGM_PARTS"] = "4"
     r = subprocess.run([sys.executable, os.path.join(HERE, "vd_volume_check.py"), str(w), str(h),
                         str(d), "9", "3"], cwd=ROOT, env=env, capture_output=True, text=True,
                        timeout=1200)

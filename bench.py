@@ -122,10 +122,31 @@ def alu_roofline(cells, ms, sm_mhz, n_sm, alu_pct):
             "ncu_alu_pipe_active_pct": alu_pct}
 
 
-def stage_roofline(nbytes, ms, peak):
+def measured_stage(config, batch, texture_scale, key):
+    """ncu DRAM bytes per step and ALU-pipe share of a stage's kernel from
+    the committed capture of the same workload (agg_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "agg_traffic.json")) as fh:
+            t = json.load(fh)
+        if (t.get("config", 5) == config and t["batch"] == batch
+                and abs(t["texture_scale"] - texture_scale) < 1e-12):
+            return t["stages"][key]
+    except Exception:
+        pass
+    return None
+
+
+def stage_roofline(nbytes, ms, peak, measured=None):
     gbs = nbytes / (ms / 1e3) / 1e9 if ms > 0 else None
-    return {"bytes_per_step": nbytes, "ms_per_step": ms, "achieved": gbs, "unit": "GB/s",
-            "frac": gbs / peak if gbs else None}
+    out = {"bytes_per_step": nbytes, "ms_per_step": ms, "achieved": gbs, "unit": "GB/s",
+           "frac": gbs / peak if gbs else None}
+    if measured and ms > 0:
+        # the bytes the kernel actually moves (ncu) over the same stage time,
+        # and its ALU-pipe share: which roofline binds it
+        out["dram_bytes_per_step"] = measured["dram_bytes_per_step"]
+        out["dram_frac"] = measured["dram_bytes_per_step"] / (ms / 1e3) / 1e9 / peak
+        out["ncu_alu_pipe_active_pct"] = measured["alu_pipe_active_pct"]
+    return out
 
 
 def traffic_line(traffic, ms, peak):
@@ -476,9 +497,11 @@ def main():
         # the other SURVEY 8(d) kernels on their algorithmic bytes
         "roofline_stages": {
             "cost": stage_roofline(2 * hw * 2 * B + 8 * hw * 2 * B + 2 * cells,
-                                   stage[2] / max(nsteps.value, 1), peak),
+                                   stage[2] / max(nsteps.value, 1), peak,
+                                   measured_stage(args.config, B, TEXTURE_SCALE, "cost")),
             "wta_variance": stage_roofline(2 * cells + 11 * hw * 2 * B,
-                                           stage[4] / max(nsteps.value, 1), peak)},
+                                           stage[4] / max(nsteps.value, 1), peak,
+                                           measured_stage(args.config, B, TEXTURE_SCALE, "wta_variance"))},
         "pipeline_roofline": {"achieved": frame_bytes / (ms_max / K / 1e3) / 1e9,
                               "frac": frame_bytes / (ms_max / K / 1e3) / 1e9 / peak},
         "gpu_launches": KERNELS_PER_STEP * K,

@@ -50,6 +50,7 @@ lines.append(f"## ncu --set full, one timed step (B={batch}), `{tag}`\n")
 lines.append("| kernel | ms | DRAM GB | DRAM % peak | warps active % | issue active % | regs | top stalls (cycles per issue) |")
 lines.append("|---|---|---|---|---|---|---|---|")
 agg_bytes, agg_ms, agg_alu = 0.0, 0.0, 0.0
+per_kernel = {}   # ncu DRAM bytes, ms and ALU-pipe share of the other hot kernels
 table = []
 for r in rows[2:]:
     d = dict(zip(hdr, r))
@@ -69,6 +70,10 @@ for r in rows[2:]:
         "_per_issue_active.ratio", ""), v) for k, v in sorted(st.items(), key=lambda kv: -kv[1])[:3])
     if ms < 0.05:
         continue   # early-exit regime variants
+    for key, pat in (("cost", "k_cost_runs"), ("wta_variance", "k_wta_runs")):
+        if pat in name:
+            per_kernel[key] = {"dram_bytes_per_step": dram, "ms_serialised": ms,
+                               "alu_pipe_active_pct": float(d["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"])}
     lines.append(f"| {name} | {ms:.2f} | {dram / 1e9:.2f} | {float(d['gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed']):.1f} | "
                  f"{float(d['sm__warps_active.avg.pct_of_peak_sustained_active']):.1f} | "
                  f"{float(d['smsp__issue_active.avg.pct_of_peak_sustained_active']):.1f} | "
@@ -81,6 +86,7 @@ with open(os.path.join(outdir, f"SUMMARY_{tag}.md"), "w") as fh:
 json.dump({"batch": batch, "texture_scale": tex, "config": 5, "dram_bytes_per_step": agg_bytes,
            "kernel_ms_per_step_serialised": agg_ms,
            "alu_pipe_active_pct": agg_alu / agg_ms if agg_ms else None,
+           "stages": per_kernel,
            "alu_source": "time-weighted sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active "
                          "over the same k_sgm_grp4 launches",
            "source": f"profiles/r01/SUMMARY_{tag}.md: sum of dram__bytes_read.sum + dram__bytes_write.sum "

@@ -72,34 +72,6 @@ TEXTURE_SCALE = 0.05
 KERNELS_PER_STEP = 19   # zmax, zidx, fill_h, fill_v, cost, 6 sgm jobs x 2 regime variants, wta, fuse
 
 
-def measured_traffic(config, batch, texture_scale):
-    """DRAM bytes per step of the aggregation stage from the committed ncu
-    capture of the same workload (profiles/r01/agg_traffic.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "agg_traffic.json")) as fh:
-            t = json.load(fh)
-        if (t.get("config", 5) == config and t["batch"] == batch
-                and abs(t["texture_scale"] - texture_scale) < 1e-12):
-            return float(t["dram_bytes_per_step"])
-    except Exception:
-        pass
-    return None
-
-
-def measured_alu(config, batch, texture_scale):
-    """ncu ALU-pipe utilisation (%) of the aggregation launches in the same
-    committed capture, or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "agg_traffic.json")) as fh:
-            t = json.load(fh)
-        if (t.get("config", 5) == config and t["batch"] == batch
-                and abs(t["texture_scale"] - texture_scale) < 1e-12):
-            return float(t["alu_pipe_active_pct"])
-    except Exception:
-        pass
-    return None
-
-
 # Integer roofline of the aggregation (SURVEY 8(d): its arithmetic intensity
 # sits above the INT/HBM ridge).  Per searched cell and path direction the
 # recurrence L = C + min(Lp(d), min(Lp(d-1), Lp(d+1)) + P1, m + P2) - m costs
@@ -120,20 +92,6 @@ def alu_roofline(cells, ms, sm_mhz, n_sm, alu_pct):
             "peak_basis": f"{n_sm} SMs x {ALU_LANES_PER_SM_CLK} ALU lanes/clk x 2 u16 per lane "
                           f"x {sm_mhz:.0f} MHz (median SM clock under load)",
             "ncu_alu_pipe_active_pct": alu_pct}
-
-
-def measured_stage(config, batch, texture_scale, key):
-    """ncu DRAM bytes per step and ALU-pipe share of a stage's kernel from
-    the committed capture of the same workload (agg_traffic.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "agg_traffic.json")) as fh:
-            t = json.load(fh)
-        if (t.get("config", 5) == config and t["batch"] == batch
-                and abs(t["texture_scale"] - texture_scale) < 1e-12):
-            return t["stages"][key]
-    except Exception:
-        pass
-    return None
 
 
 def stage_roofline(nbytes, ms, peak, measured=None):
@@ -175,38 +133,59 @@ def sequence_specs(n, seed0):
 
 def render_frames(specs, frames, device, rig=None, with_gt=False):
     """Device images [len(frames)][B][2][H][W] (torch uint8); with ``with_gt``
-    also the rendered ground-truth disparities (float64, same shape)."""
+    also the rendered ground-truth disparities (float64, same shape).
+    ``specs`` are either (boxes, poses, motions) tuples (texture seed
+    17 + index) or ``scenes.ConfigSequence`` objects (their own per-frame
+    boxes and texture seeds); the device renderer's bytes equal the
+    reference's synth.render_frame (tests/test_gpu_render.py)."""
     import torch
     from paper_1708_06301_b200 import _lib
     from paper_1708_06301_b200.core import StereoRig
-    rig = rig or StereoRig(**RIG)
+    cfgseq = hasattr(specs[0], "boxes")
+    if rig is None:
+        rig = StereoRig(**specs[0].rig) if cfgseq else StereoRig(**RIG)
     h, w = rig.height, rig.width
     rs = _lib.rig_struct(rig)
     B = len(specs)
-    n_box = specs[0][0].shape[0]
-    boxes = np.ascontiguousarray(np.stack([sp[0] for sp in specs]), np.float64)
-    seeds = np.arange(B, dtype=np.int64) + 17
+    if cfgseq:
+        seeds = np.array([cs.texture_seed for cs in specs], np.int64)
+        scale, bg = specs[0].texture_scale, specs[0].background
+    else:
+        seeds = np.arange(B, dtype=np.int64) + 17
+        scale, bg = TEXTURE_SCALE, 12
     out = torch.empty((len(frames), B, 2, h, w), dtype=torch.uint8, device=device)
     gt = (torch.empty((len(frames), B, 2, h, w), dtype=torch.float64, device=device)
           if with_gt else None)
     stream = torch.cuda.current_stream(device).cuda_stream
     for i, k in enumerate(frames):
-        poses = np.ascontiguousarray(np.stack([sp[1][k % SEQ_FRAMES] for sp in specs]), np.float64)
-        _lib.call("es_render", ctypes.byref(rs), _lib.ptr(boxes), n_box, _lib.ptr(poses),
-                  _lib.ptr(seeds), B, ctypes.c_double(TEXTURE_SCALE), 12,
+        if cfgseq:
+            boxes = np.ascontiguousarray(np.stack([cs.boxes[k % cs.n_frames] for cs in specs]),
+                                         np.float64)
+            poses = np.stack([cs.poses[k % cs.n_frames] for cs in specs])
+        else:
+            boxes = np.ascontiguousarray(np.stack([sp[0] for sp in specs]), np.float64)
+            poses = np.stack([sp[1][k % SEQ_FRAMES] for sp in specs])
+        poses = np.ascontiguousarray(poses, np.float64)
+        _lib.call("es_render", ctypes.byref(rs), _lib.ptr(boxes), boxes.shape[1], _lib.ptr(poses),
+                  _lib.ptr(seeds), B, ctypes.c_double(scale), bg,
                   ctypes.c_void_p(out[i].data_ptr()),
                   ctypes.c_void_p(gt[i].data_ptr()) if with_gt else None, ctypes.c_void_p(stream))
     torch.cuda.synchronize(device)
     return (out, gt) if with_gt else out
 
 
+def _motions(sp):
+    return sp.motions if hasattr(sp, "motions") else sp[2]
+
+
 def motions_for_frames(specs, k0, k1):
     """Motions of sequence 0's frames k0 .. k1-1 (None for frame 0)."""
-    return [specs[0][2][k % SEQ_FRAMES] for k in range(k0, k1)]
+    m = _motions(specs[0])
+    return [m[k % len(m)] for k in range(k0, k1)]
 
 
 def motions_for(specs, k):
-    return [sp[2][k % SEQ_FRAMES] for sp in specs]
+    return [_motions(sp)[k % len(_motions(sp))] for sp in specs]
 
 
 # ----------------------------------------------------------------- clocks
@@ -249,54 +228,185 @@ class Clocks:
                 "samples": len(sm)}
 
 
-# ----------------------------------------------------------------- CPU port
+# ----------------------------------------------------------------- CPU arms
+#
+# The reference arm and cpu_baseline run the UNMODIFIED reference package
+# (installed into baseline/_ref by `pip install --no-deps --target
+# baseline/_ref /root/reference/pkg`) through its
+# own public API: synth.render_frame renders the inputs and
+# DisparityPipeline.process_frame runs the frames.  Nothing here imports the
+# product package or loads its .so: the worker processes are spawned fresh
+# and only read the numpy-only scene definitions (scenes.py) by file path.
+# Without baseline/_ref (a checkout that never ran the install) they fall
+# back to the numpy oracle port (kind "port").
 
-def _cpu_worker(args):
-    # spawned: the module globals are config 5's, so the rig travels with the job
-    frames, motions, rig = args
-    import oracle as O
-    orc = O.OracleStereo(rig["f"], rig["b"], rig["cx"], rig["cy"], rig["width"], rig["height"],
-                         rig["d_max"])
-    orc.step(frames[0][0], frames[0][1], None)          # full-range frame 0: warm-up
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_available():
+    return os.path.isdir(os.path.join(REF_PATH, "egostereo"))
+
+
+def load_scenes():
+    """paper_1708_06301_b200/scenes.py as a standalone module (numpy only;
+    the package and its CUDA library are not imported)."""
+    import importlib.util
+    name = "_bench_scenes"
+    if name in sys.modules:
+        return sys.modules[name]
+    spec = importlib.util.spec_from_file_location(
+        name, os.path.join(ROOT, "paper_1708_06301_b200", "scenes.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[name] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def _ref_worker(job):
+    """One CPU process: render sequence `seq` of `config` with the
+    reference's synth, run frame 0 (full range, untimed), then time
+    `n_timed` predicted frames through DisparityPipeline.process_frame."""
+    config, seq, n_timed, kind = job
+    scenes = load_scenes()
+    cs = scenes.config_sequence(config, seq, n_frames=max(n_timed + 1, 2))
+    if kind == "reference":
+        sys.path.insert(0, REF_PATH)
+        from egostereo import core, pipeline, synth
+        rig = core.StereoRig(**cs.rig)
+        frames = []
+        for k in range(n_timed + 1):
+            scene = synth.SceneSpec(rig=rig, primitives=[synth.Box(*map(float, b))
+                                                         for b in cs.boxes[k]],
+                                    texture_seed=cs.texture_seed,
+                                    texture_scale=cs.texture_scale, background=cs.background)
+            l, r, _, _ = synth.render_frame(scene, cs.poses[k])
+            pair = scenes.apply_salt(np.stack([l.data, r.data]), cs, k)
+            frames.append((core.GrayImage(pair[0]), core.GrayImage(pair[1])))
+        pipe = pipeline.DisparityPipeline(rig)
+        step = lambda k: pipe.process_frame(frames[k][0], frames[k][1], cs.motions[k])  # noqa: E731
+    else:
+        sys.path.insert(0, ROOT)
+        import oracle as O
+        r = cs.rig
+        orc = O.OracleStereo(r["f"], r["b"], r["cx"], r["cy"], r["width"], r["height"], r["d_max"])
+        imgs = _port_render(cs, n_timed + 1)
+        step = lambda k: orc.step(imgs[k][0], imgs[k][1], cs.motions[k])  # noqa: E731
+    step(0)                                   # full-range frame 0: warm-up
     t0 = time.perf_counter()
-    for k in range(1, len(frames)):
-        orc.step(frames[k][0], frames[k][1], motions[k])
+    for k in range(1, n_timed + 1):
+        step(k)
     return time.perf_counter() - t0
 
 
+def _port_render(cs, n):
+    """Fallback inputs for the port arm (no reference installed): the
+    oracle's own restatement of synth.render_frame is not part of the port,
+    so render with a scalar numpy ray caster of the same scene."""
+    sys.path.insert(0, ROOT)
+    from oracle.egostereo_oracle import render_boxes
+    return [render_boxes(cs, k) for k in range(n)]
+
+
 def default_cpu_procs():
-    """Every host core the process may use, bounded by memory (the numpy
-    port needs ~1.1 GB per 1242x375 frame step)."""
+    """Every host core the process may use, bounded by memory (the
+    reference needs ~1.5 GB per 1242x375 frame step)."""
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     try:
         mem_gb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2**30
-        cores = max(1, min(cores, int(mem_gb / 1.5)))
+        cores = max(1, min(cores, int(mem_gb / 2.0)))
     except (ValueError, OSError, AttributeError):
         pass
     return cores
 
 
-def cpu_baseline(imgs, specs, procs, n_timed=1):
-    """numpy oracle port: P single-threaded processes, each its own sequence:
-    one full-range warm-up frame (not timed) then ``n_timed`` predicted
-    frames; frames/s = P * n_timed / slowest process."""
-    P = min(procs, len(specs))
-    jobs = [([(imgs[k, s, 0], imgs[k, s, 1]) for k in range(n_timed + 1)],
-             [motions_for(specs, k)[s] for k in range(n_timed + 1)], RIG) for s in range(P)]
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+def cpu_arm(config, procs, n_timed, seq0=0):
+    """P single-threaded processes, each its own sequence: one untimed
+    full-range frame, then ``n_timed`` timed predicted frames; frames/s =
+    P * n_timed / slowest process."""
+    kind = "reference" if reference_available() else "port"
+    P = max(1, procs)
+    jobs = [(config, seq0 + s, n_timed, kind) for s in range(P)]
+    os.environ["OMP_NUM_THREADS"] = "1"
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
     t0 = time.perf_counter()
     with mp.get_context("spawn").Pool(P) as pool:
-        per = pool.map(_cpu_worker, jobs)
+        per = pool.map(_ref_worker, jobs)
     wall = time.perf_counter() - t0
     fps = P * n_timed / max(per)
-    return {"value": fps, "unit": "frames/s", "cores": P, "kind": "port",
-            "sample": f"{P} sequences x {n_timed} predicted frame(s) ({W}x{H}, D={D_MAX + 1}) in "
-                      f"{P} parallel single-threaded processes; per-process {min(per):.1f}-"
-                      f"{max(per):.1f} s; wall {wall:.0f} s incl. the untimed full-range frame"}
+    c = CONFIGS[config]
+    what = ("the unmodified reference (baseline/_ref egostereo: synth.render_frame inputs, "
+            "DisparityPipeline.process_frame)" if kind == "reference" else
+            "the numpy oracle port (baseline/_ref not installed)")
+    return {"value": fps, "unit": "frames/s", "cores": P, "kind": kind,
+            "sample": f"{what}: {P} sequences x {n_timed} predicted frame(s) "
+                      f"({c['W']}x{c['H']}, D={c['d_max'] + 1}) in {P} parallel single-threaded "
+                      f"processes; per-process {min(per):.1f}-{max(per):.1f} s; wall {wall:.0f} s "
+                      f"incl. rendering and the untimed full-range frame 0"}
 
 
 # ----------------------------------------------------------------- main
+
+def lib_sha256():
+    import hashlib
+    path = os.path.join(ROOT, "paper_1708_06301_b200", "libegostereo_b200.so")
+    try:
+        with open(path, "rb") as fh:
+            return hashlib.sha256(fh.read()).hexdigest()
+    except OSError:
+        return None
+
+
+def measured_ncu(config, batch, texture_scale):
+    """ncu numbers (DRAM bytes and ALU-pipe share per stage and step) of the
+    SAME library build and workload, from profiles/ncu_traffic.json (written
+    by tools/ncu_traffic.py from an `ncu --set full` capture of this bench);
+    entries whose library hash differs from the loaded .so are stale and
+    ignored, so a kernel change can never report another build's traffic."""
+    sha = lib_sha256()
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            entries = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    for t in entries:
+        if (t.get("lib_sha256") == sha and t.get("config") == config and t.get("batch") == batch
+                and abs(t.get("texture_scale", -1) - texture_scale) < 1e-12):
+            return t
+    return None
+
+
+def relaunch(args_list, n):
+    """`bench.py --gpus N` outside torchrun: re-launch as N ranks (one
+    process per GPU) through torch.distributed.run on 127.0.0.1."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + args_list
+    return subprocess.call(cmd)
+
+
+def reference_arm(args, config_line):
+    """--impl reference: the reference's own CPU implementation on the
+    box's host cores (rank 0 only), same metric / unit / config."""
+    K, Wm = args.steps, max(args.warmup, 3)
+    # bounded sample: each timed step = one predicted frame of every
+    # process's sequence; at most 5 steps (a 1242x375 reference frame takes
+    # ~15-20 s per core), config 4 one step (a 2048x1024 D=256 frame takes
+    # minutes and ~10 GB per process)
+    nt = min(K, 5) if args.config == 5 else 1
+    procs = args.cpu_procs if args.config == 5 else min(args.cpu_procs, 2)
+    cb = cpu_arm(args.config, procs, nt)
+    print(json.dumps({
+        "impl": "reference", "metric": "frames/s", "value": cb["value"], "unit": "frames/s",
+        "n_gpus": args.gpus, "steps": K, "warmup": Wm, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u16+f64", "data": "synthetic",
+        "config": config_line, "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
 
 def main():
     ap = argparse.ArgumentParser()
@@ -307,7 +417,8 @@ def main():
                     help="BASELINE.json config: 5 (headline, 1242x375 D=128) or 4 "
                          "(2048x1024 D=256)")
     ap.add_argument("--batch", type=int, default=None,
-                    help="sequences per GPU (default: config 5: 64, config 4: 8)")
+                    help="sequences over ALL GPUs, split evenly (strong scaling; default: "
+                         "config 5: 64, config 4: 8)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-procs", type=int, default=default_cpu_procs())
     ap.add_argument("--no-cpu", action="store_true")
@@ -315,59 +426,45 @@ def main():
     ap.add_argument("--full-range", action="store_true",
                     help="PipelineParams(baseline=True): every frame full range (the config-1 "
                          "workload per frame; tuning aid, not the headline)")
-    ap.add_argument("--texture-scale", type=float, default=TEXTURE_SCALE,
-                    help="world-space texture lattice (m); 0.05 gives paper-like ~50%% "
-                         "search fractions, 0.2 gives ~10%%")
     args = ap.parse_args()
-    globals()["TEXTURE_SCALE"] = args.texture_scale
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(relaunch(sys.argv[1:], args.gpus))
     use_config(args.config)
     if args.batch is None:
         args.batch = CFG["batch"]
-    if args.config == 4:
-        # a 2048x1024 D=256 numpy frame needs several GB and minutes per process
-        args.cpu_procs = min(args.cpu_procs, 2)
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.batch % world:
+        raise SystemExit(f"--batch {args.batch} must divide evenly over {world} GPUs")
+    B = args.batch // world
+    K, Wm = args.steps, max(args.warmup, 3)
+    if Wm + K > SEQ_FRAMES:
+        raise SystemExit(f"warmup + steps must be <= {SEQ_FRAMES} (sequence length)")
+    config = {"workload": CFG["workload"], "sequences_total": args.batch,
+              "batch_per_gpu": B, "height": H, "width": W, "d_max": D_MAX,
+              "texture_scale": TEXTURE_SCALE,
+              "l2": "no flush needed: the working set per step (ragged volumes of all "
+                    "sequences, GBs) is far larger than the 126 MB L2"}
 
-    from paper_1708_06301_b200 import sharding
-    rank, world, local = sharding.world()
+    if args.impl == "reference":
+        # no product import on this arm
+        if rank == 0:
+            reference_arm(args, config)
+        return
+
     import torch
     import torch.distributed as dist
+    from paper_1708_06301_b200 import _lib, pipeline, scenes, sharding
+    from paper_1708_06301_b200.core import StereoRig
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
 
-    K, Wm, B = args.steps, max(args.warmup, 3), args.batch
-    if Wm + K > SEQ_FRAMES:
-        raise SystemExit(f"warmup + steps must be <= {SEQ_FRAMES} (sequence length)")
-    config = {"workload": CFG["workload"],
-              "batch_per_gpu": B, "height": H, "width": W, "d_max": D_MAX,
-              "l2": "working set per step (ragged volumes of all sequences) >> 126 MB L2"}
-
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        # each timed step = one predicted frame of every process's sequence
-        specs = sequence_specs(args.cpu_procs, seed0=5000)
-        # (config 4: one predicted frame -- a 2048x1024 D=256 numpy step takes minutes)
-        # bounded: at most 10 predicted frames per process (about 2 minutes)
-        nt = min(K, 10) if args.config == 5 else 1
-        imgs = render_frames(specs, list(range(nt + 1)), device).cpu().numpy()
-        cb = cpu_baseline(imgs, specs, args.cpu_procs, n_timed=nt)
-        print(json.dumps({
-            "impl": "reference", "metric": "frames/s", "value": cb["value"], "unit": "frames/s",
-            "n_gpus": args.gpus, "steps": K, "warmup": Wm, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u16+f64", "data": "synthetic",
-            "config": config, "cpu_baseline": cb,
-            "e2e": {"value": cb["value"], "unit": "frames/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}))
-        return
-
-    from paper_1708_06301_b200 import _lib, pipeline
-    from paper_1708_06301_b200.core import StereoRig
-
     rig = StereoRig(**RIG)
-    seeds = sharding.rank_sequences(rank, world, B, seed0=1000)
-    specs = sequence_specs(B, seed0=seeds[0])
+    seqs = sharding.rank_sequences(rank, world, B, seed0=0)    # global sequence indices
+    specs = [scenes.config_sequence(args.config, s) for s in seqs]
     frames = list(range(Wm + K))
     imgs = render_frames(specs, frames, device)
     bp = pipeline.BatchedPipeline(rig, B, pipeline.PipelineParams(baseline=args.full_range),
@@ -375,12 +472,14 @@ def main():
     eng = bp.engine
     ext = torch.cuda.ExternalStream(eng.stream(), device=device)
 
-    # warm-up: frame 0 (full range) .. Wm-1, synced so have_state is known
-    for k in range(Wm):
-        bp.process_frames(None, motions_for(specs, k), sync=True, images_dev=imgs[k].data_ptr())
+    def warm_up():
+        # frame 0 (full range) .. Wm-1, synced so have_state is known
+        for k in range(Wm):
+            bp.process_frames(None, motions_for(specs, k), sync=True,
+                              images_dev=imgs[k].data_ptr())
 
-    # ---- device-resident timed region ---------------------------------
-    _lib.call("es_ctx_profile", eng._h, 1)
+    # ---- device-resident timed region (per-stage profiling OFF) ---------
+    warm_up()
     acc = ctypes.c_uint64()
     _lib.call("es_ctx_cells_acc", eng._h, ctypes.byref(acc), 1)   # reset the accumulator
     clocks = Clocks(local) if rank == 0 else None
@@ -389,7 +488,6 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(ext):
         ev0.record()
-    cells = 0
     for i in range(K):
         k = Wm + i
         bp.process_frames(None, motions_for(specs, k), sync=False,
@@ -400,17 +498,26 @@ def main():
     torch.cuda.synchronize(device)
     ms = ev0.elapsed_time(ev1)
     clk = clocks.stop() if clocks else None
+    _lib.call("es_ctx_cells_acc", eng._h, ctypes.byref(acc), 1)
+    cells = acc.value / K           # searched cells per step (all sequences, both views)
+    ms_max = sharding.max_over_ranks(ms, device)
+    frames_total = args.batch * K
+    value = frames_total / (ms_max / 1e3)
+
+    # ---- stage split: a second, untimed replay of the same frames with
+    # per-stage CUDA events (es_ctx_profile) on the context's stream
+    bp.reset()
+    warm_up()
+    _lib.call("es_ctx_profile", eng._h, 1)
+    for i in range(K):
+        bp.process_frames(None, motions_for(specs, Wm + i), sync=False,
+                          images_dev=imgs[Wm + i].data_ptr())
+    bp.sync()
     stage = np.zeros(6)
     nsteps = ctypes.c_int64()
     _lib.call("es_ctx_stage_times", eng._h, _lib.ptr(stage), ctypes.byref(nsteps))
     _lib.call("es_ctx_profile", eng._h, 0)
-    # searched cells summed over the timed steps (all sequences, both views),
-    # averaged per step for the byte model
-    _lib.call("es_ctx_cells_acc", eng._h, ctypes.byref(acc), 1)
-    cells = acc.value / K
-    ms_max = sharding.max_over_ranks(ms, device)
-    frames_total = B * K * world
-    value = frames_total / (ms_max / 1e3)
+    st_ms = stage / max(nsteps.value, 1)
 
     # ---- quality (untimed): fused left maps of the last timed frame against
     # the renderer's ground truth, evaluated on the device (metrics.py)
@@ -457,64 +564,65 @@ def main():
         torch.cuda.synchronize(device)
         te = sharding.max_over_ranks(e0.elapsed_time(e1), device)
         e2e = {"value": frames_total / (te / 1e3), "unit": "frames/s",
-               "h2d_bytes_per_step": int(B * 2 * H * W), "d2h_bytes_per_step": int(B * H * W * 2)}
+               "h2d_bytes_per_step": int(B * 2 * H * W), "d2h_bytes_per_step": int(B * H * W * 2),
+               "per": "rank (each GPU copies its own B sequences)"}
 
-    # ---- roofline of the dominant kernel (aggregation stage) ------------
+    # ---- rooflines (SURVEY 8(d) algorithmic bytes / CUDA-event stage times)
     peak, peak_kind = peaks()
-    agg_ms = stage[3] / max(nsteps.value, 1)
+    ncu = measured_ncu(args.config, B, TEXTURE_SCALE)
+    nst = (ncu or {}).get("stages", {})
+    agg_ms = st_ms[3]
     hw = H * W
     agg_bytes = 4 * cells + 8 * hw * 2 * B
     achieved = agg_bytes / (agg_ms / 1e3) / 1e9
     frame_bytes = 8 * cells + 106 * hw * 2 * B
     stage_names = ["predict", "intervals", "cost", "aggregate", "wta_variance", "checks_fuse"]
+    sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
+    agg_ncu = nst.get("aggregate")
     line = {
         "metric": "frames/s", "value": value, "unit": "frames/s", "n_gpus": world,
         "steps": K, "warmup": Wm, "ms_per_step": ms_max / K, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u16+f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "u16+f64", "data": "synthetic",
         "config": config,
+        "per_rank_batch": B,
         "mde_per_s": value * hw * (D_MAX + 1) / 1e6,
         "searched_mcells_per_s": cells * world / (ms_max / K / 1e3) / 1e6,
         "search_fraction": cells / (2 * B * hw * (D_MAX + 1)),
-        "stage_ms_per_step": {n: stage[i] / max(nsteps.value, 1) for i, n in enumerate(stage_names)},
-        "roofline": {"bound": "hbm", "kernel": "sgm aggregation (4 family launches)",
+        "stage_ms_per_step": {n: st_ms[i] for i, n in enumerate(stage_names)},
+        "stage_timing": "second untimed replay of the same frames with per-stage CUDA events "
+                        "(the headline is timed with stage events off)",
+        "roofline": {"bound": "hbm", "kernel": "sgm aggregation (k_sgm_grp4 jobs)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
-                     # ncu DRAM bytes of the same stage per step (committed capture of
-                     # this workload), vs bytes_per_step algorithmic
-                     "traffic": measured_traffic(args.config, B, TEXTURE_SCALE),
-                     "traffic_unit": "bytes per step (all sequences, both views)",
+                     "traffic": agg_ncu["dram_bytes_per_step"] if agg_ncu else None,
+                     "traffic_unit": "ncu DRAM bytes per step (all sequences, both views), "
+                                     "same library build (sha256 match) or null",
                      "peak_kind": peak_kind, "bytes_per_step": agg_bytes,
                      "floor_ms": agg_bytes / (peak * 1e9) * 1e3},
-        # the multi-pass aggregation reads C and read-modify-writes a partial
-        # sum once per direction: its DRAM traffic / stage time is the
-        # bandwidth it actually sustains
-        "aggregation_dram": traffic_line(measured_traffic(args.config, B, TEXTURE_SCALE), agg_ms, peak),
-        # the same stage against the integer pipe: its HBM floor (bytes_per_step
-        # / peak) is below its ALU floor, so the ALU pipe is the binding roofline
-        "roofline_int": alu_roofline(cells, agg_ms, (clk or {}).get("sm_mhz") or 1965.0,
+        "aggregation_dram": traffic_line(agg_ncu["dram_bytes_per_step"] if agg_ncu else None,
+                                         agg_ms, peak),
+        "roofline_int": alu_roofline(cells, agg_ms, sm_mhz,
                                      torch.cuda.get_device_properties(device).multi_processor_count,
-                                     measured_alu(args.config, B, TEXTURE_SCALE)),
-        # the other SURVEY 8(d) kernels on their algorithmic bytes
+                                     agg_ncu["alu_pipe_active_pct"] if agg_ncu else None),
         "roofline_stages": {
-            "cost": stage_roofline(2 * hw * 2 * B + 8 * hw * 2 * B + 2 * cells,
-                                   stage[2] / max(nsteps.value, 1), peak,
-                                   measured_stage(args.config, B, TEXTURE_SCALE, "cost")),
-            "wta_variance": stage_roofline(2 * cells + 11 * hw * 2 * B,
-                                           stage[4] / max(nsteps.value, 1), peak,
-                                           measured_stage(args.config, B, TEXTURE_SCALE, "wta_variance"))},
+            "cost": stage_roofline(2 * hw * 2 * B + 8 * hw * 2 * B + 2 * cells, st_ms[2], peak,
+                                   nst.get("cost")),
+            "wta_variance": stage_roofline(2 * cells + 11 * hw * 2 * B, st_ms[4], peak,
+                                           nst.get("wta_variance"))},
         "pipeline_roofline": {"achieved": frame_bytes / (ms_max / K / 1e3) / 1e9,
                               "frac": frame_bytes / (ms_max / K / 1e3) / 1e9 / peak},
+        "ncu_provenance": ({"lib_sha256": ncu["lib_sha256"], "capture": ncu.get("capture")}
+                           if ncu else "no ncu capture of this library build"),
         "gpu_launches": KERNELS_PER_STEP * K,
         "quality": quality,
         "clocks": clk,
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
-        specs_c = sequence_specs(args.cpu_procs, seed0=1000)
-        imgs_c = render_frames(specs_c, [0, 1], device).cpu().numpy()
-        line["cpu_baseline"] = cpu_baseline(imgs_c, specs_c, args.cpu_procs, n_timed=1)
+        line["cpu_baseline"] = cpu_arm(args.config, args.cpu_procs if args.config == 5 else
+                                       min(args.cpu_procs, 2), 1)
     if rank == 0:
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

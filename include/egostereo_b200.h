@@ -173,9 +173,18 @@ int es_bad_pixel_counts(const double* est, const uint8_t* est_valid, const doubl
 int es_ctx_metrics(es_ctx* ctx, int view, const double* gt_dev, const uint8_t* gt_valid_dev,
                    int64_t gt_stride, int mode, uint64_t* counts);
 
-/* ---- synthetic input renderer (synth.py:87-218 restated, boxes only) ---- */
-/* boxes [n_seq][n_box][6], poses [n_seq][16], seeds [n_seq]; out_dev images
- * [n_seq][2][H][W] (device); gt_dev optional [n_seq][2][H][W] f64 (device) */
+/* ---- synthetic input renderer (synth.py:87-218 restated bit-exactly) -----
+ * Not on the hot path: generates the bench / parity inputs on the device;
+ * its bytes equal synth.render_frame's (tests/test_gpu_render.py).
+ * prims [n_seq][n_prim][8] records: [0, x0, x1, y0, y1, z0, z1, 0] = Box
+ * (synth.py:41-50); [1, z, x0, x1, y0, y1, 0, flags] = Plane (synth.py:27-38),
+ * flags bits 0..3 = bound x0, x1, y0, y1 present (None otherwise);
+ * poses [n_seq][16] world-from-camera, seeds [n_seq] texture seeds; out_dev
+ * images [n_seq][2][H][W] (device); gt_dev optional [n_seq][2][H][W] f64 */
+int es_render_prims(const es_rig* rig, const double* prims, int n_prim, const double* poses,
+                    const int64_t* seeds, int n_seq, double texture_scale, int background,
+                    uint8_t* out_dev, double* gt_dev, void* stream);
+/* boxes only: boxes [n_seq][n_box][6] (x0, x1, y0, y1, z0, z1) */
 int es_render(const es_rig* rig, const double* boxes, int n_box, const double* poses,
               const int64_t* seeds, int n_seq, double texture_scale, int background,
               uint8_t* out_dev, double* gt_dev, void* stream);

@@ -39,6 +39,7 @@ __all__ = [
     "fill_holes",
     "OracleStereo",
     "PATH_ORDER",
+    "render_boxes",
 ]
 
 
@@ -529,3 +530,72 @@ class OracleStereo:
             out[v + "_fraction"] = float((hi - lo + 1).sum() / (lo.size * (D + 1)))
         self.frame += 1
         return out
+
+
+# --------------------------------------------------------------- renderer
+# synth.py:87-218 restated for axis-aligned boxes (the bench scenes): only
+# the bench's port-fallback CPU arm (no reference installed) uses it, to
+# build its inputs; pinned against synth.render_frame's own output in
+# tests/test_oracle_golden.py::test_render_boxes_matches_reference_synth.
+
+def _lattice(ix, iy, iz, seed):
+    """synth.py:87-103 (uint64 splitmix-style finaliser)."""
+    u = np.uint64
+    with np.errstate(over="ignore"):
+        h = ix.astype(np.int64).view(u) * u(0x9E3779B97F4A7C15)
+        h ^= iy.astype(np.int64).view(u) * u(0xC2B2AE3D27D4EB4F)
+        h ^= iz.astype(np.int64).view(u) * u(0x165667B19E3779F9)
+        h ^= u(seed & 0xFFFFFFFFFFFFFFFF) * u(0x27D4EB2F165667C5)
+        for sh, mul in ((30, 0xBF58476D1CE4E5B9), (27, 0x94D049BB133111EB)):
+            h ^= h >> u(sh)
+            h *= u(mul)
+        h ^= h >> u(31)
+    return (h >> u(11)).astype(np.float64) / float(1 << 53)
+
+
+def _noise(q, seed):
+    """synth.py:106-120: trilinear value noise, corners summed in order."""
+    base = np.floor(q)
+    fr = q - base
+    fr = fr * fr * (3.0 - 2.0 * fr)
+    bi = base.astype(np.int64)
+    acc = np.zeros(q.shape[:-1])
+    for c in range(8):
+        o = [(c >> k) & 1 for k in range(3)]
+        w = [fr[..., k] if o[k] else 1.0 - fr[..., k] for k in range(3)]
+        acc += _lattice(bi[..., 0] + o[0], bi[..., 1] + o[1], bi[..., 2] + o[2], seed) * w[0] * w[1] * w[2]
+    return acc
+
+
+def render_boxes(cs, k):
+    """(2, H, W) uint8 images of frame k of a scenes.ConfigSequence
+    (synth.render_frame, synth.py:195-218, for Box primitives)."""
+    r = cs.rig
+    h, w, f = r["height"], r["width"], r["f"]
+    pose = np.asarray(cs.poses[k], np.float64)
+    R, c0 = pose[:3, :3], pose[:3, 3]
+    ys, xs = np.mgrid[0:h, 0:w]
+    dc = np.stack([(xs - r["cx"]) / f, (ys - r["cy"]) / f, np.ones((h, w))], axis=-1)
+    dirs = dc @ R.T                      # BLAS, as synth.py:175
+    out = []
+    for c in (c0, c0 + R @ np.array([r["b"], 0.0, 0.0])):
+        tb = np.full((h, w), np.inf)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            for bx in cs.boxes[k]:
+                tn, tf = np.full((h, w), -np.inf), np.full((h, w), np.inf)
+                for ax in range(3):
+                    d = dirs[..., ax]
+                    inv = np.where(d != 0.0, 1.0 / d, np.inf)
+                    t1, t2 = (bx[2 * ax] - c[ax]) * inv, (bx[2 * ax + 1] - c[ax]) * inv
+                    inside = (c[ax] >= bx[2 * ax]) & (c[ax] <= bx[2 * ax + 1])
+                    lo = np.where(d == 0.0, -np.inf if inside else np.inf, np.minimum(t1, t2))
+                    hi = np.where(d == 0.0, np.inf if inside else -np.inf, np.maximum(t1, t2))
+                    tn, tf = np.maximum(tn, lo), np.minimum(tf, hi)
+                tb = np.minimum(tb, np.where((tn <= tf) & (tn > 1e-6), tn, np.inf))
+        hit = np.isfinite(tb)
+        pts = c + np.where(hit, tb, 0.0)[..., None] * dirs
+        q = pts / cs.texture_scale
+        v = 0.65 * _noise(q, cs.texture_seed) + 0.35 * _noise(2.0 * q, cs.texture_seed + 1)
+        tex = 20.0 + 215.0 * np.clip(v, 0.0, 1.0)
+        out.append(np.clip(np.rint(np.where(hit, tex, float(cs.background))), 0, 255).astype(np.uint8))
+    return np.stack(out)

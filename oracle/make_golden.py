@@ -280,6 +280,51 @@ def gen_sequences():
     save("render", **out)
 
 
+def prim_records(primitives):
+    """synth primitives -> the device renderer's [n][8] records
+    (include/egostereo_b200.h es_render_prims)."""
+    out = []
+    for p in primitives:
+        if isinstance(p, synth.Plane):
+            flags = sum(1 << i for i, b in enumerate((p.x0, p.x1, p.y0, p.y1)) if b is not None)
+            out.append([1.0, p.z] + [0.0 if b is None else b for b in (p.x0, p.x1, p.y0, p.y1)]
+                       + [0.0, float(flags)])
+        else:
+            out.append([0.0, p.x0, p.x1, p.y0, p.y1, p.z0, p.z1, 0.0])
+    return np.asarray(out, np.float64)
+
+
+def gen_render_planes():
+    """synth.render_frame on scenes mixing bounded / unbounded fronto-parallel
+    planes and boxes, under rotated poses, both views: the device renderer
+    must reproduce the images and ground truth bit for bit."""
+    from scipy.spatial.transform import Rotation
+    out = {}
+    rng = np.random.default_rng(23)
+    for case, (w, h, f) in enumerate([(96, 48, 64.0), (161, 77, 120.0), (310, 94, 180.0)]):
+        rig = rig_small(w, h, min(w - 1, 60), f=f, b=0.5)
+        prims = [synth.Plane(z=9.0),
+                 synth.Plane(z=4.0, x0=-1.0, x1=0.4, y0=None, y1=0.6),
+                 synth.Plane(z=3.0, x0=None, x1=-0.5, y0=-0.8, y1=None),
+                 synth.Box(x0=0.2, x1=1.1, y0=-0.3, y1=0.7, z0=2.2, z1=2.9),
+                 synth.Box(x0=-2.0, x1=2.0, y0=0.9, y1=1.0, z0=1.0, z1=8.0)]
+        scene = synth.SceneSpec(rig=rig, primitives=prims, texture_seed=40 + case,
+                                texture_scale=[None, 0.03, 0.05][case])
+        for k in range(2):
+            R = Rotation.from_rotvec(rng.normal(0, 0.03, 3)).as_matrix()
+            pose = core.make_motion(R, rng.normal(0, 0.1, 3))
+            l, r, gl, gr = synth.render_frame(scene, pose)
+            out[f"c{case}_f{k}_pose"] = pose
+            out[f"c{case}_f{k}_img"] = np.stack([l.data, r.data])
+            out[f"c{case}_f{k}_gt"] = np.stack([gl.values, gr.values])
+        out[f"c{case}_rig"] = np.array([rig.f, rig.b, rig.cx, rig.cy, rig.width, rig.height,
+                                        rig.d_max])
+        out[f"c{case}_prims"] = prim_records(prims)
+        out[f"c{case}_seed"] = np.array(scene.texture_seed)
+        out[f"c{case}_scale"] = np.array(scene.texture_scale)
+    save("render_planes", **out)
+
+
 def gen_config1():
     """Config 1 at full size (1242x375, D=128): compact reference outputs."""
     left, right, gt = scenes.config1_pair(seed=1000)
@@ -475,3 +520,5 @@ if __name__ == "__main__":
         gen_kitti()
     if "acceptance" in which:
         gen_acceptance()
+    if "render_planes" in which:
+        gen_render_planes()

@@ -83,6 +83,7 @@ SIGNATURES = {
     "es_reject_edges": [_P, _P, _I, _I, _D, _I, _P],
     "es_warp_points": [_P, _P, _I, _P],
     "es_render": [_P, _P, _I, _P, _P, _I, _D, _I, _P, _P, _P],
+    "es_render_prims": [_P, _P, _I, _P, _P, _I, _D, _I, _P, _P, _P],
     "es_bad_pixel_counts": [_P, _P, _P, _P, _L, _I, _I, _P, _P, _P],
     "es_ctx_metrics": [_P, _I, _P, _P, _L, _I, _P],
 }

@@ -1234,25 +1234,36 @@ int es_warp_points(const double* Hm, const double* pts, int n, double* out) {
   return ES_OK;
 }
 
-int es_render(const es_rig* rig, const double* boxes, int n_box, const double* poses,
-              const int64_t* seeds, int n_seq, double texture_scale, int background,
-              uint8_t* out_dev, double* gt_dev, void* stream) {
+int es_render_prims(const es_rig* rig, const double* prims, int n_prim, const double* poses,
+                    const int64_t* seeds, int n_seq, double texture_scale, int background,
+                    uint8_t* out_dev, double* gt_dev, void* stream) {
   Scratch s;
   RenderArgs a;
   a.rig = to_rig(rig);
-  a.boxes = s.up(boxes, (size_t)n_seq * n_box * 6);
-  a.n_box = n_box;
+  a.prims = s.up(prims, (size_t)n_seq * n_prim * 8);
+  a.n_prim = n_prim;
   a.poses = s.up(poses, (size_t)n_seq * 16);
   a.seeds = (const long long*)s.up(seeds, (size_t)n_seq);
   a.texture_scale = texture_scale;
   a.background = background;
   a.img = out_dev;
   a.gt = gt_dev;
-  NEED(a.boxes && a.poses && a.seeds);
+  NEED(a.prims && a.poses && a.seeds);
   launch_render(a, n_seq, (cudaStream_t)stream);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize((cudaStream_t)stream));
   return ES_OK;
+}
+
+int es_render(const es_rig* rig, const double* boxes, int n_box, const double* poses,
+              const int64_t* seeds, int n_seq, double texture_scale, int background,
+              uint8_t* out_dev, double* gt_dev, void* stream) {
+  if (n_box < 0 || n_seq < 0) return fail(ES_ERR_VALUE, "es_render: negative count");
+  std::vector<double> prims((size_t)n_seq * n_box * 8, 0.0);
+  for (size_t k = 0; k < (size_t)n_seq * n_box; ++k)
+    for (int j = 0; j < 6; ++j) prims[8 * k + 1 + j] = boxes[6 * k + j];
+  return es_render_prims(rig, prims.data(), n_box, poses, seeds, n_seq, texture_scale,
+                         background, out_dev, gt_dev, stream);
 }
 
 }  // extern "C"

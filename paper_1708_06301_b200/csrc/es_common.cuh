@@ -71,10 +71,22 @@ __device__ __forceinline__ long long np_to_i64(double v) {
   return (long long)v;
 }
 
-// Warp a pixel through a disparity-space homography exactly as the oracle
-// does (geometry.py:95-159): explicit k = 0..3 dot products, no FMA (the
-// translation unit is compiled with -fmad=false).  Returns false when the
-// fourth homogeneous component vanishes (PointAtInfinityError).
+// The reference's (N,K) @ (K,M) float64 products (``hom @ H.T``,
+// geometry.py:110; ``dir_cam @ R.T``, synth.py:175) run through OpenBLAS
+// dgemm, whose kernel accumulates k = 0, 1, ... with fused multiply-adds:
+// acc = a0*b0; acc = fma(a_k, b_k, acc).  Measured bit-exact against numpy
+// in the build container (OpenBLAS 0.3.30, Haswell kernel) on 10^6 points;
+// the TU is otherwise compiled with -fmad=false, so every other a*b+c rounds
+// twice as numpy's elementwise ops do.
+__device__ __forceinline__ double dgemm_dot3(double a0, double b0, double a1, double b1,
+                                             double a2, double b2) {
+  return __fma_rn(a2, b2, __fma_rn(a1, b1, __dmul_rn(a0, b0)));
+}
+
+// Warp a pixel through a disparity-space homography exactly as the reference
+// does (geometry.py:95-159): hom = (x-cx, y-cy, d, 1), out = hom @ H.T in
+// dgemm order (the k = 3 term is fma(1, h3, acc) = acc + h3).  Returns
+// false when the fourth homogeneous component vanishes (PointAtInfinityError).
 __device__ __forceinline__ bool warp_point(const double* __restrict__ Hm, double x, double y,
                                            double d, double cx, double cy, double& xp,
                                            double& yp, double& dp) {
@@ -82,7 +94,8 @@ __device__ __forceinline__ bool warp_point(const double* __restrict__ Hm, double
   double o[4];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
-    o[r] = ((Hm[4 * r + 0] * px + Hm[4 * r + 1] * py) + Hm[4 * r + 2] * d) + Hm[4 * r + 3];
+    o[r] = __dadd_rn(dgemm_dot3(px, Hm[4 * r + 0], py, Hm[4 * r + 1], d, Hm[4 * r + 2]),
+                     Hm[4 * r + 3]);
   if (fabs(o[3]) < 1e-12) return false;
   xp = o[0] / o[3] + cx;
   yp = o[1] / o[3] + cy;

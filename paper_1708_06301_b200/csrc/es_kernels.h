@@ -169,8 +169,8 @@ void launch_metrics(const MetricsArgs& a, int n_maps, cudaStream_t st);
 // ---- synthetic renderer (es_render.cu) -------------------------------------
 struct RenderArgs {
   Rig rig;
-  const double* boxes;   // [n_seq][n_box][6]
-  int n_box;
+  const double* prims;   // [n_seq][n_prim][8]: kind, 6 parameters, plane bound flags
+  int n_prim;
   const double* poses;   // [n_seq][16] world-from-camera (left camera)
   const long long* seeds;  // [n_seq] texture seed
   double texture_scale;

@@ -1,12 +1,18 @@
 // Synthetic stereo renderer for the benchmark sequences (configs 2-5).
 //
-// Restates the reference's ray caster (synth.py:87-218) for axis-aligned
-// boxes: per-pixel rays through the rectified pinhole rig, slab intersection
-// (synth.py:130-170), two-octave value-noise texture with the splitmix-style
-// uint64 lattice hash (synth.py:87-127), background intensity where nothing
-// is hit, and exact ground-truth disparity f*b/Z.  This is input generation
-// (off the hot path): it replaces ~1.5 s/frame of numpy
-// ray casting so 64-sequence runs are practical on the GPU box.
+// Restates the reference's ray caster (synth.py:87-218) bit-exactly:
+// per-pixel rays through the rectified pinhole rig, whose world directions
+// ``dir_cam @ R.T`` (synth.py:175) are formed in OpenBLAS dgemm order
+// (dgemm_dot3, es_common.cuh); fronto-parallel planes, optionally bounded
+// (synth.py:27-38,147-163), and axis-aligned boxes by slab intersection
+// (synth.py:41-50,130-170); the two-octave value-noise texture with the
+// splitmix-style uint64 lattice hash (synth.py:87-127); background intensity
+// where nothing is hit; ground-truth disparity f*b/Z.  Every other float64
+// operation is one IEEE op in numpy's order (the TU is built -fmad=false).
+// This is input generation, off the hot path: it
+// replaces ~1.5 s/frame of numpy ray casting, and because its bytes equal
+// synth.render_frame's, the bench and the full-size parity tests consume
+// exactly the images the reference renders (tests/test_gpu_render.py).
 #include "es_common.cuh"
 #include "es_kernels.h"
 
@@ -59,6 +65,33 @@ __device__ __forceinline__ void slab(double c, double d, double lo, double hi, d
   tmax = fmax(t1, t2);
 }
 
+// one primitive record: [kind, p0..p5, flags]
+//   kind 0 box:   x0 x1 y0 y1 z0 z1
+//   kind 1 plane: z x0 x1 y0 y1 -, flags bit 0..3 = x0 x1 y0 y1 present
+__device__ __forceinline__ double intersect(const double* pr, const double* o, const double* d) {
+  if (pr[0] != 0.0) {
+    const double dz = d[2];
+    double t = (pr[1] - o[2]) / dz;
+    if (fabs(dz) < 1e-15) t = INFINITY;
+    const double px = o[0] + t * d[0];
+    const double py = o[1] + t * d[1];
+    const int fl = (int)pr[7];
+    bool ok = t > 1e-6;
+    if (fl & 1) ok &= px >= pr[2];
+    if (fl & 2) ok &= px <= pr[3];
+    if (fl & 4) ok &= py >= pr[4];
+    if (fl & 8) ok &= py <= pr[5];
+    return ok ? t : INFINITY;
+  }
+  double t0x, t1x, t0y, t1y, t0z, t1z;
+  slab(o[0], d[0], pr[1], pr[2], t0x, t1x);
+  slab(o[1], d[1], pr[3], pr[4], t0y, t1y);
+  slab(o[2], d[2], pr[5], pr[6], t0z, t1z);
+  const double tn = fmax(fmax(t0x, t0y), t0z);
+  const double tf = fmin(fmin(t1x, t1y), t1z);
+  return (tn <= tf && tn > 1e-6) ? tn : INFINITY;
+}
+
 __global__ void k_render(RenderArgs a) {
   const int W = a.rig.W, H = a.rig.H;
   const size_t HW = (size_t)W * H;
@@ -66,25 +99,17 @@ __global__ void k_render(RenderArgs a) {
   if (i >= (int)HW) return;
   const int seq = blockIdx.y >> 1, view = blockIdx.y & 1;
   const double* T = a.poses + 16 * seq;
-  const double* boxes = a.boxes + (size_t)seq * a.n_box * 6;
+  const double* prims = a.prims + (size_t)seq * a.n_prim * 8;
   const int x = i % W, y = i / W;
-  const double dc[3] = {((double)x - a.rig.cx) / a.rig.f, ((double)y - a.rig.cy) / a.rig.f, 1.0};
+  const double dcx = ((double)x - a.rig.cx) / a.rig.f, dcy = ((double)y - a.rig.cy) / a.rig.f;
   double dir[3], cen[3];
   for (int r = 0; r < 3; ++r) {
-    dir[r] = (T[4 * r + 0] * dc[0] + T[4 * r + 1] * dc[1]) + T[4 * r + 2] * dc[2];
+    dir[r] = dgemm_dot3(dcx, T[4 * r + 0], dcy, T[4 * r + 1], 1.0, T[4 * r + 2]);
+    // c_right = c_left + R @ (b, 0, 0): the zero terms are exact
     cen[r] = T[4 * r + 3] + (view ? T[4 * r + 0] * a.rig.b : 0.0);
   }
   double tbest = INFINITY;
-  for (int k = 0; k < a.n_box; ++k) {
-    const double* bx = boxes + 6 * k;
-    double t0x, t1x, t0y, t1y, t0z, t1z;
-    slab(cen[0], dir[0], bx[0], bx[1], t0x, t1x);
-    slab(cen[1], dir[1], bx[2], bx[3], t0y, t1y);
-    slab(cen[2], dir[2], bx[4], bx[5], t0z, t1z);
-    const double tn = fmax(fmax(t0x, t0y), t0z);
-    const double tf = fmin(fmin(t1x, t1y), t1z);
-    if (tn <= tf && tn > 1e-6) tbest = fmin(tbest, tn);
-  }
+  for (int k = 0; k < a.n_prim; ++k) tbest = fmin(tbest, intersect(prims + 8 * k, cen, dir));
   const bool hit = isfinite(tbest);
   double inten = (double)a.background;
   if (hit) {

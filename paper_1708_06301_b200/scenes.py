@@ -17,7 +17,8 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["fbm_texture", "config1_pair", "box_scene", "sequence_spec"]
+__all__ = ["fbm_texture", "config1_pair", "box_scene", "sequence_spec", "CONFIG_RIGS",
+           "ConfigSequence", "config_sequence", "apply_salt", "TEXTURE_SCALE", "BACKGROUND"]
 
 
 def fbm_texture(h: int, w: int, rng, octaves: int = 5, period: float = 24.0):
@@ -80,13 +81,14 @@ def config1_pair(seed: int = 1000, width: int = 1242, height: int = 375,
     return left, right, gt
 
 
-def box_scene(rng, n_boxes: int = 8, z_range=(5.0, 60.0)):
+def box_scene(rng, n_boxes: int = 8, z_range=(5.0, 60.0), ground_z1: float = 90.0,
+              wall_z: float = 95.0):
     """Ground slab, n seeded boxes and a far wall (configs 2-5).
 
     Returns a float64 array (n, 6) of boxes (x0, x1, y0, y1, z0, z1); the far
     wall is a very thin box.  World frame: x right, y down, z forward."""
-    boxes = [(-60.0, 60.0, 1.65, 1.8, 3.0, 90.0),      # ground slab
-             (-400.0, 400.0, -200.0, 200.0, 95.0, 95.5)]  # far wall
+    boxes = [(-60.0, 60.0, 1.65, 1.8, 3.0, ground_z1),      # ground slab
+             (-400.0, 400.0, -200.0, 200.0, wall_z, wall_z + 0.5)]  # far wall
     for _ in range(n_boxes):
         z0 = float(rng.uniform(*z_range))
         depth = float(rng.uniform(0.5, 3.0))
@@ -110,11 +112,12 @@ def _rot(yaw, pitch, roll):
 
 def sequence_spec(seed: int, n_frames: int, step: float = 1.0,
                   step_sigma: float = 0.05, yaw_deg: float = 0.5,
-                  tilt_deg: float = 0.1, n_boxes: int = 8, z_range=(5.0, 60.0)):
+                  tilt_deg: float = 0.1, n_boxes: int = 8, z_range=(5.0, 60.0),
+                  ground_z1: float = 90.0, wall_z: float = 95.0):
     """Scene boxes plus world-from-camera poses and relative motions
     (frame k-1 -> k, the reference's ``relative_motion``)."""
     rng = np.random.default_rng(seed)
-    boxes = box_scene(rng, n_boxes, z_range)
+    boxes = box_scene(rng, n_boxes, z_range, ground_z1, wall_z)
     poses = []
     pos = np.zeros(3)
     yaw = pitch = roll = 0.0
@@ -131,3 +134,92 @@ def sequence_spec(seed: int, n_frames: int, step: float = 1.0,
         poses.append(T)
     motions = [None] + [np.linalg.inv(poses[k]) @ poses[k - 1] for k in range(1, n_frames)]
     return boxes, poses, motions
+
+
+# ----------------------------------------------------------------------------
+# BASELINE.json configs 2-5 as concrete seeded sequences.  One definition
+# serves the bench (config 5, and config 4 via --config 4), the full-size
+# parity tests and the golden generator (oracle/make_golden_configs.py), which
+# renders the same scenes with the reference's own synth.render_frame: the
+# device renderer is bit-exact with it, so every consumer sees identical bytes.
+
+TEXTURE_SCALE = 0.05   # world lattice (m): paper-like ~50% search fractions
+BACKGROUND = 12
+TEXTURE_SEED0 = 17     # texture seed of sequence s = TEXTURE_SEED0 + s
+
+_RIG_S = dict(f=718.9, b=0.54, cx=607.0, cy=185.0, width=1242, height=375, d_max=127)
+CONFIG_RIGS = {
+    2: _RIG_S, 3: _RIG_S, 5: _RIG_S,
+    4: dict(f=1400.0, b=0.3, cx=1023.5, cy=511.5, width=2048, height=1024, d_max=255),
+}
+# scene seed of sequence s = seed0 + s
+CONFIG_SEQS = {
+    2: dict(frames=10, step=1.0, yaw_deg=0.5, seed0=2000),
+    # 100 frames at 1 m/frame: the static scene extends to 160 m (boxes), 250 m
+    # (ground) and 260 m (wall) so the camera never drives out of it; three
+    # extra boxes move on their own (forward 0.3-1.5 m/frame, lateral drift),
+    # violating the ego-motion prediction; 2% salt noise per view and frame.
+    3: dict(frames=100, step=1.0, yaw_deg=0.5, seed0=3000, z_range=(5.0, 160.0),
+            ground_z1=250.0, wall_z=260.0, movers=3, salt=0.02),
+    4: dict(frames=30, step=1.5, yaw_deg=1.0, seed0=4000),
+    5: dict(frames=50, step=1.0, yaw_deg=0.5, seed0=1000),
+}
+
+
+class ConfigSequence:
+    """One seeded sequence of a BASELINE config: ``boxes[k]`` (n, 6) per
+    frame, world-from-camera ``poses[k]``, relative ``motions[k]`` (None for
+    frame 0), texture seed, salt-noise rate and seed."""
+
+    def __init__(self, config, seq, rig, boxes, poses, motions, texture_seed, salt, salt_seed):
+        self.config, self.seq, self.rig = config, seq, rig
+        self.boxes, self.poses, self.motions = boxes, poses, motions
+        self.texture_seed = texture_seed
+        self.texture_scale = TEXTURE_SCALE
+        self.background = BACKGROUND
+        self.salt, self.salt_seed = salt, salt_seed
+
+    @property
+    def n_frames(self):
+        return len(self.poses)
+
+
+def config_sequence(config: int, seq: int = 0, n_frames: int | None = None) -> ConfigSequence:
+    c = CONFIG_SEQS[config]
+    n = c["frames"] if n_frames is None else n_frames
+    kw = {k: c[k] for k in ("z_range", "ground_z1", "wall_z") if k in c}
+    boxes, poses, motions = sequence_spec(seed=c["seed0"] + seq, n_frames=n, step=c["step"],
+                                          yaw_deg=c["yaw_deg"], **kw)
+    per_frame = [boxes] * n
+    movers = c.get("movers", 0)
+    if movers:
+        rng = np.random.default_rng(c["seed0"] + seq + 7777)
+        start = []
+        for _ in range(movers):
+            z0 = float(rng.uniform(8.0, 40.0))
+            wdt, hgt, dep = (float(rng.uniform(0.8, 2.5)), float(rng.uniform(0.8, 2.0)),
+                             float(rng.uniform(0.5, 2.0)))
+            xc = float(rng.uniform(-4.0, 4.0))
+            start.append((xc - wdt / 2, xc + wdt / 2, 1.65 - hgt, 1.65, z0, z0 + dep))
+        start = np.asarray(start, np.float64)
+        vel = np.stack([rng.uniform(-0.08, 0.08, movers), np.zeros(movers),
+                        rng.uniform(0.3, 1.5, movers)], axis=1)
+        per_frame = []
+        for k in range(n):
+            mv = start.copy()
+            mv[:, 0:2] += (vel[:, 0] * k)[:, None]
+            mv[:, 4:6] += (vel[:, 2] * k)[:, None]
+            per_frame.append(np.concatenate([boxes, mv]))
+    return ConfigSequence(config, seq, CONFIG_RIGS[config], per_frame, poses, motions,
+                          TEXTURE_SEED0 + seq, c.get("salt", 0.0), c["seed0"] + seq + 31337)
+
+
+def apply_salt(pair: np.ndarray, cs: ConfigSequence, frame: int) -> np.ndarray:
+    """Salt noise of config 3: each pixel of each view independently set to
+    255 with probability ``cs.salt`` (seeded per sequence and frame).
+    Modifies and returns ``pair`` (2, H, W) uint8."""
+    if cs.salt > 0.0:
+        rng = np.random.default_rng([cs.salt_seed, frame])
+        for v in range(2):
+            pair[v][rng.random(pair[v].shape) < cs.salt] = 255
+    return pair

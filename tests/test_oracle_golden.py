@@ -136,3 +136,18 @@ def test_metrics():
                                   g[f"c{case}_{mode}_rates"]), (case, mode)
             assert np.array_equal(O.bad_mask(est, ev, gt, gv, mode), g[f"c{case}_{mode}_mask"])
             assert np.array_equal(O.error_rgb(est, ev, gt, gv, mode), g[f"c{case}_{mode}_rgb"])
+
+
+def test_render_boxes_matches_reference_synth():
+    """The oracle's restated ray caster (the bench's port-fallback inputs)
+    against synth.render_frame's own output (golden render.npz)."""
+    from types import SimpleNamespace
+    g = load_golden("render")
+    f, b, cx, cy, w, h, d_max = g["rig"]
+    cs = SimpleNamespace(rig=dict(f=f, b=b, cx=cx, cy=cy, width=int(w), height=int(h)),
+                         poses=[g["pose0"], g["pose1"]], boxes=[g["boxes"]] * 2,
+                         texture_scale=float(g["texture_scale"]),
+                         texture_seed=int(g["texture_seed"]), background=int(g["background"]))
+    for k in range(2):
+        img = O.render_boxes(cs, k)
+        assert np.array_equal(img[0], g[f"img{k}_l"]) and np.array_equal(img[1], g[f"img{k}_r"])

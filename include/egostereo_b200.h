@@ -152,6 +152,14 @@ int es_fill_zoom_holes(const double* d, const double* p, const uint8_t* valid, i
 int es_reject_edges(const double* d, const uint8_t* valid, int H, int W, double gamma_e,
                     int edge_window, uint8_t* out);
 
+/* sgm._box_sum (sgm.py:130-136): exact integer (2r+1)^2 window sums with
+ * edge replication, a (H, W) -> out (H, W) */
+int es_box_sum(const int64_t* a, int H, int W, int radius, int64_t* out);
+/* sgm.matching_variance (sgm.py:287-316): the scalar float64 walk over one
+ * pixel's n interval costs from index center */
+int es_matching_variance_scalar(const double* costs, int n, int center, double s_max,
+                                double r_min, double* r);
+
 /* geometry.warp_point (geometry.py:95-115) on n principal-point-relative
  * (x, y, d) triples; out (n, 3) */
 int es_warp_points(const double* Hm, const double* pts, int n, double* out);

@@ -82,6 +82,8 @@ SIGNATURES = {
     "es_fill_zoom_holes": [_P, _P, _P, _I, _I, _D, _D, _P, _P, _P],
     "es_reject_edges": [_P, _P, _I, _I, _D, _I, _P],
     "es_warp_points": [_P, _P, _I, _P],
+    "es_box_sum": [_P, _I, _I, _I, _P],
+    "es_matching_variance_scalar": [_P, _I, _I, _D, _D, _P],
     "es_render": [_P, _P, _I, _P, _P, _I, _D, _I, _P, _P, _P],
     "es_render_prims": [_P, _P, _I, _P, _P, _I, _D, _I, _P, _P, _P],
     "es_bad_pixel_counts": [_P, _P, _P, _P, _L, _I, _I, _P, _P, _P],

@@ -1217,6 +1217,75 @@ int es_reject_edges(const double* d, const uint8_t* valid, int H, int W, double 
   return ES_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// sgm._box_sum (sgm.py:130-136): exact integer window sums over a
+// (2r+1)^2 window with edge replication; one thread per output
+__global__ void k_box_sum(const long long* a, int H, int W, int r, long long* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= H * W) return;
+  const int x = i % W, y = i / W;
+  long long s = 0;
+  for (int dy = -r; dy <= r; ++dy) {
+    const long long* row = a + (size_t)min(max(y + dy, 0), H - 1) * W;
+    for (int dx = -r; dx <= r; ++dx) s += row[min(max(x + dx, 0), W - 1)];
+  }
+  out[i] = s;
+}
+
+// sgm.matching_variance (sgm.py:287-316), the scalar walk in float64 over
+// one pixel's interval costs: rel = c - c[center]; count neighbours while the
+// running sum stays below s_max, outward on each side (one thread)
+__global__ void k_variance_scalar(const double* c, int n, int center, double s_max,
+                                  double r_min, double* out) {
+  const double cs = c[center];
+  int cnt = 0;
+  double s = 0.0;
+  for (int i = center - 1; i >= 0; --i) {
+    s += c[i] - cs;
+    if (s >= s_max) break;
+    ++cnt;
+  }
+  s = 0.0;
+  for (int i = center + 1; i < n; ++i) {
+    s += c[i] - cs;
+    if (s >= s_max) break;
+    ++cnt;
+  }
+  *out = fmax((double)cnt, r_min);
+}
+}  // namespace
+
+extern "C" {
+
+int es_box_sum(const int64_t* a, int H, int W, int radius, int64_t* out) {
+  if (H < 1 || W < 1 || radius < 0) return fail(ES_ERR_VALUE, "box_sum: bad shape or radius");
+  const size_t n = (size_t)H * W;
+  Scratch s;
+  long long* da = (long long*)s.up(a, n);
+  long long* dout = s.get<long long>(n);
+  NEED(da && dout);
+  k_box_sum<<<(unsigned)((n + 255) / 256), 256>>>(da, H, W, radius, dout);
+  DONE();
+  CK(cudaMemcpy(out, dout, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
+  return ES_OK;
+}
+
+int es_matching_variance_scalar(const double* costs, int n, int center, double s_max,
+                                double r_min, double* r) {
+  if (n < 1 || center < 0 || center >= n)
+    return fail(ES_ERR_VALUE, "selected disparity outside the interval");
+  Scratch s;
+  double* dc = s.up(costs, (size_t)n);
+  double* dr = s.get<double>(1);
+  NEED(dc && dr);
+  k_variance_scalar<<<1, 1>>>(dc, n, center, s_max, r_min, dr);
+  DONE();
+  CK(cudaMemcpy(r, dr, sizeof(double), cudaMemcpyDeviceToHost));
+  return ES_OK;
+}
+
 int es_warp_points(const double* Hm, const double* pts, int n, double* out) {
   Scratch s;
   double* dH = s.up(Hm, 16);

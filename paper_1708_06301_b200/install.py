@@ -1,0 +1,276 @@
+"""Drop-in installation into the reference package ``egostereo`` (INTEGRATION.md
+Option B).
+
+    import egostereo
+    from paper_1708_06301_b200 import install
+    install.install(egostereo)        # every hot-path name now runs on the B200
+    ...
+    install.uninstall(egostereo)      # restore the numpy implementations
+
+The reference has no plugin system: its operator API is its Python function
+surface, and it binds the stage functions by name three times -- in the
+defining modules (``sgm``, ``prediction``, ``fusion``, ``geometry``,
+``metrics``), again in ``pipeline`` (pipeline.py:38-50) and again in the
+package root (__init__.py:30-47).  ``install`` rebinds every one of those
+names to an adapter that runs this package's device implementation and
+returns the REFERENCE's own types (``egostereo.core.DisparityMap``,
+``egostereo.sgm.CostVolume`` ...), so isinstance checks, dataclass equality
+and attribute access behave exactly as before.  Device errors are re-raised
+as the reference's exception classes (``egostereo.geometry.
+PointAtInfinityError``; ValueError / RuntimeError otherwise), with the
+message the device produced.
+
+``DisparityPipeline`` becomes a subclass of the reference class whose state
+lives on the device (one ``es_ctx`` per pipeline); ``process_frame`` returns
+a reference ``FrameResult`` built from the device maps, and ``run_sequence``
+/ ``cli`` pick it up through the rebound name.
+
+Nothing here imports ``egostereo`` unless it is asked to; the product never
+depends on the reference.
+"""
+
+from __future__ import annotations
+
+import functools
+import importlib
+
+import numpy as np
+
+from . import errors as _errors
+from . import fusion as _fusion
+from . import geometry as _geometry
+from . import metrics as _metrics
+from . import pipeline as _pipeline
+from . import prediction as _prediction
+from . import sgm as _sgm
+
+__all__ = ["install", "uninstall", "installed", "REBOUND"]
+
+# module -> names rebound there (the defining modules of the reference)
+REBOUND = {
+    "sgm": ("search_intervals", "matching_cost", "aggregate_paths", "select_disparity",
+            "matching_variance", "matching_variance_map", "lr_consistency", "sad_check",
+            "_box_sum"),
+    "prediction": ("reject_edges", "_predict_view", "predict_maps", "fill_zoom_holes"),
+    "fusion": ("fuse_maps",),
+    "geometry": ("warp_point", "warp_pixels"),
+    "metrics": ("bad_pixel_rate", "bad_pixel_mask", "density", "error_image",
+                "search_space_fraction"),
+}
+# names the reference re-binds at import time (pipeline.py:38-50, __init__.py:30-47)
+PIPELINE_NAMES = ("fuse_maps", "fill_zoom_holes", "predict_maps", "aggregate_paths",
+                  "lr_consistency", "matching_cost", "matching_variance_map", "sad_check",
+                  "search_intervals", "select_disparity")
+ROOT_NAMES = ("fuse_maps", "warp_point", "bad_pixel_rate", "search_space_fraction",
+              "predict_maps", "search_intervals")
+
+_OURS = {"sgm": _sgm, "prediction": _prediction, "fusion": _fusion, "geometry": _geometry,
+         "metrics": _metrics}
+_SAVED_ATTR = "_b200_saved_bindings"
+
+
+def _mods(ref):
+    return {name: importlib.import_module(f"{ref.__name__}.{name}")
+            for name in ("core", "sgm", "prediction", "fusion", "geometry", "metrics", "pipeline")}
+
+
+class _Convert:
+    """Our boundary types -> the reference's (same fields, fresh objects)."""
+
+    def __init__(self, m):
+        self.m = m
+
+    def disp(self, d):
+        return self.m["core"].DisparityMap(np.asarray(d.values), np.asarray(d.valid))
+
+    def var(self, v):
+        return self.m["core"].VarianceMap(np.asarray(v.values))
+
+    def state(self, s, frame=None):
+        return self.m["core"].FilterState(self.disp(s.left), self.var(s.left_var),
+                                          self.disp(s.right), self.var(s.right_var),
+                                          frame=s.frame if frame is None else frame)
+
+    def intervals(self, iv):
+        return self.m["sgm"].IntervalMap(np.asarray(iv.lo), np.asarray(iv.hi), int(iv.d_max))
+
+    def badpix(self, r):
+        return self.m["metrics"].BadPixelResult(**{k: getattr(r, k) for k in
+                                                   ("rate", "rate_all", "density")})
+
+
+def _reraise(m):
+    """Map the package's device exceptions onto the reference's classes."""
+    pai = m["geometry"].PointAtInfinityError
+
+    def deco(fn):
+        @functools.wraps(fn)
+        def wrapper(*a, **kw):
+            try:
+                return fn(*a, **kw)
+            except _errors.PointAtInfinityError as e:
+                raise pai(str(e)) from None
+        return wrapper
+    return deco
+
+
+def _adapters(m):
+    cv = _Convert(m)
+    rr = _reraise(m)
+    s, p, f, g, mt = _sgm, _prediction, _fusion, _geometry, _metrics
+    ad = {"sgm": {}, "prediction": {}, "fusion": {}, "geometry": {}, "metrics": {}}
+    ad["sgm"]["search_intervals"] = lambda d, pv, rig: cv.intervals(s.search_intervals(d, pv, rig))
+    ad["sgm"]["matching_cost"] = lambda left, right, iv, prm, view="left": m["sgm"].CostVolume(
+        s.matching_cost(left, right, iv, prm, view).data, iv)
+    ad["sgm"]["aggregate_paths"] = lambda vol, prm: m["sgm"].CostVolume(
+        s.aggregate_paths(vol, prm).data, vol.intervals)
+    ad["sgm"]["select_disparity"] = lambda agg: cv.disp(s.select_disparity(agg))
+    ad["sgm"]["matching_variance"] = s.matching_variance
+    ad["sgm"]["matching_variance_map"] = lambda agg, d, prm: cv.var(
+        s.matching_variance_map(agg, d, prm))
+    ad["sgm"]["lr_consistency"] = s.lr_consistency
+    ad["sgm"]["sad_check"] = s.sad_check
+    ad["sgm"]["_box_sum"] = s._box_sum
+    ad["prediction"]["reject_edges"] = p.reject_edges
+
+    def _pv(disp, var, H, rig, params):
+        d, v = p._predict_view(disp, var, H, rig, params)
+        return cv.disp(d), cv.var(v)
+    ad["prediction"]["_predict_view"] = _pv
+    ad["prediction"]["predict_maps"] = lambda st, T, rig, prm: cv.state(
+        p.predict_maps(st, T, rig, prm))
+
+    def _fill(disp, var, gamma_f, q):
+        d, v = p.fill_zoom_holes(disp, var, gamma_f, q)
+        return cv.disp(d), cv.var(v)
+    ad["prediction"]["fill_zoom_holes"] = _fill
+
+    def _fuse(dp, pp, dm, rm, prm):
+        d, v = f.fuse_maps(dp, pp, dm, rm, prm)
+        return cv.disp(d), cv.var(v)
+    ad["fusion"]["fuse_maps"] = _fuse
+    ad["geometry"]["warp_point"] = g.warp_point
+    ad["geometry"]["warp_pixels"] = g.warp_pixels
+    ad["metrics"]["bad_pixel_rate"] = lambda e, t, mode="or": cv.badpix(mt.bad_pixel_rate(e, t, mode))
+    ad["metrics"]["bad_pixel_mask"] = mt.bad_pixel_mask
+    ad["metrics"]["density"] = mt.density
+    ad["metrics"]["error_image"] = mt.error_image
+    ad["metrics"]["search_space_fraction"] = mt.search_space_fraction
+    for mod in ad:
+        for name, fn in ad[mod].items():
+            ad[mod][name] = rr(fn)
+            ad[mod][name].__b200__ = True
+    return ad
+
+
+def _device_pipeline_class(m):
+    """A subclass of the reference DisparityPipeline whose filter state lives
+    on the device (pipeline.py:90-170)."""
+    ref_cls = m["pipeline"].DisparityPipeline
+    cv = _Convert(m)
+    pai = m["geometry"].PointAtInfinityError
+
+    class DisparityPipeline(ref_cls):
+        __doc__ = ref_cls.__doc__
+        __b200__ = True
+
+        def __init__(self, rig, params=None):
+            self.rig = rig
+            self.params = params or m["pipeline"].PipelineParams()
+            self._dev = _pipeline.DisparityPipeline(rig, self.params)
+
+        @property
+        def state(self):
+            st = self._dev.state
+            return cv.state(st)
+
+        @state.setter
+        def state(self, value):
+            # the reference constructor / reset assign an empty state; the
+            # device context owns the state, so only resets are meaningful
+            if value is not None and not np.asarray(value.left.valid).any() \
+                    and not np.asarray(value.right.valid).any():
+                self._dev.reset()
+                return
+            raise AttributeError("the device pipeline's filter state is owned by the device; "
+                                 "use reset()")
+
+        def reset(self):
+            self._dev.reset()
+
+        def process_frame(self, left, right, motion=None):
+            try:
+                res = self._dev.process_frame(left, right, motion)
+            except _errors.PointAtInfinityError as e:
+                raise pai(str(e)) from None
+            fused = res.fused
+            return m["pipeline"].FrameResult(
+                frame=res.frame,
+                predicted_left=cv.disp(res.predicted_left),
+                predicted_left_var=cv.var(res.predicted_left_var),
+                predicted_right=cv.disp(res.predicted_right),
+                predicted_right_var=cv.var(res.predicted_right_var),
+                intervals_left=cv.intervals(res.intervals_left),
+                intervals_right=cv.intervals(res.intervals_right),
+                measured_left=cv.disp(res.measured_left),
+                measured_left_var=cv.var(res.measured_left_var),
+                measured_right=cv.disp(res.measured_right),
+                measured_right_var=cv.var(res.measured_right_var),
+                keep_left=np.asarray(res.keep_left, bool),
+                keep_right=np.asarray(res.keep_right, bool),
+                fused=m["core"].FilterState(cv.disp(fused.left), cv.var(fused.left_var),
+                                            cv.disp(fused.right), cv.var(fused.right_var),
+                                            frame=res.frame),
+                search_fraction_left=res.search_fraction_left,
+                search_fraction_right=res.search_fraction_right)
+
+    DisparityPipeline.__name__ = DisparityPipeline.__qualname__ = "DisparityPipeline"
+    DisparityPipeline.__module__ = ref_cls.__module__
+    return DisparityPipeline
+
+
+def installed(ref) -> bool:
+    return hasattr(ref, _SAVED_ATTR)
+
+
+def install(ref=None):
+    """Rebind every hot-path name of the reference package ``ref`` (default:
+    ``import egostereo``) to the device implementation.  Idempotent."""
+    if ref is None:
+        ref = importlib.import_module("egostereo")
+    if installed(ref):
+        return ref
+    m = _mods(ref)
+    ad = _adapters(m)
+    saved = []
+
+    def bind(mod, name, value):
+        saved.append((mod, name, getattr(mod, name)))
+        setattr(mod, name, value)
+
+    for modname, names in REBOUND.items():
+        for name in names:
+            bind(m[modname], name, ad[modname][name])
+    flat = {name: fn for mod in ad.values() for name, fn in mod.items()}
+    for name in PIPELINE_NAMES:
+        bind(m["pipeline"], name, flat[name])
+    for name in ROOT_NAMES:
+        bind(ref, name, flat[name])
+    dp = _device_pipeline_class(m)
+    bind(m["pipeline"], "DisparityPipeline", dp)
+    bind(ref, "DisparityPipeline", dp)
+    setattr(ref, _SAVED_ATTR, saved)
+    return ref
+
+
+def uninstall(ref=None):
+    """Restore the bindings ``install`` replaced."""
+    if ref is None:
+        ref = importlib.import_module("egostereo")
+    saved = getattr(ref, _SAVED_ATTR, None)
+    if saved is None:
+        return ref
+    for mod, name, value in reversed(saved):
+        setattr(mod, name, value)
+    delattr(ref, _SAVED_ATTR)
+    return ref

@@ -21,7 +21,8 @@ from .core import DisparityMap, VarianceMap
 
 __all__ = ["SgmParams", "IntervalMap", "CostVolume", "full_range_intervals",
            "search_intervals", "matching_cost", "aggregate_paths", "select_disparity",
-           "matching_variance", "matching_variance_map", "lr_consistency", "sad_check"]
+           "matching_variance", "matching_variance_map", "lr_consistency", "sad_check",
+           "_box_sum"]
 
 _BORDER_INTENSITY_COST = 255
 _VIEWS = {"left": 0, "right": 1}
@@ -150,13 +151,29 @@ def select_disparity(aggregated) -> DisparityMap:
     return DisparityMap(d, v.astype(bool))
 
 
+def _box_sum(a, radius: int) -> np.ndarray:
+    """Exact integer window sums with edge replication (sgm.py:130-136),
+    on the device; int64 (H, W) like the reference."""
+    a = np.ascontiguousarray(np.asarray(a).astype(np.int64))
+    if a.ndim != 2:
+        raise ValueError("_box_sum expects a 2-D array")
+    out = np.empty_like(a)
+    _lib.call("es_box_sum", _lib.ptr(a), a.shape[0], a.shape[1], int(radius), _lib.ptr(out))
+    return out
+
+
 def matching_variance_map(aggregated, disp, params) -> VarianceMap:
-    """Outward cost-budget walk from the winner (sgm.py:319-344)."""
+    """Outward cost-budget walk from the winner (sgm.py:319-344).  Like the
+    reference (``disp.values.astype(np.int64)``, sgm.py:326) the winners are
+    truncated toward zero, so fractional maps are accepted."""
     data = _lib.c_array(aggregated.data, np.float32)
     h, w, D = data.shape
     lo = _lib.c_array(aggregated.intervals.lo, np.int64)
     hi = _lib.c_array(aggregated.intervals.hi, np.int64)
-    d = _lib.c_array(disp.values, np.float64)
+    d = np.asarray(disp.values, dtype=np.float64).astype(np.int64).astype(np.float64)
+    if d.size and (d.min() < 0 or d.max() >= D):
+        raise IndexError(f"winners outside [0, {D}) for a volume of {D} planes")
+    d = np.ascontiguousarray(d)
     r = np.empty((h, w), np.float64)
     _lib.call("es_matching_variance_map", _lib.ptr(data), _lib.ptr(lo), _lib.ptr(hi), _lib.ptr(d),
               h, w, D, ctypes.c_double(params.s_max), ctypes.c_double(params.r_min), _lib.ptr(r))
@@ -164,19 +181,16 @@ def matching_variance_map(aggregated, disp, params) -> VarianceMap:
 
 
 def matching_variance(costs, lo: int, d_star: int, params) -> float:
-    """Scalar form over one pixel's interval costs (sgm.py:287-316)."""
-    costs = np.asarray(costs, dtype=np.float64).ravel()
+    """Scalar form over one pixel's interval costs (sgm.py:287-316): the
+    float64 walk, one device thread."""
+    costs = np.ascontiguousarray(np.asarray(costs, dtype=np.float64).ravel())
     center = d_star - lo
     if not 0 <= center < costs.size:
         raise ValueError(f"selected disparity {d_star} outside interval starting at {lo}")
-    D = lo + costs.size
-    vol = np.full((1, 1, D), np.inf, np.float32)
-    vol[0, 0, lo:] = costs
-    iv = IntervalMap(np.array([[lo]]), np.array([[D - 1]]), D - 1)
-    r = matching_variance_map(CostVolume(vol, iv),
-                              DisparityMap(np.array([[float(d_star)]]), np.array([[True]])),
-                              params)
-    return float(r.values[0, 0])
+    r = ctypes.c_double()
+    _lib.call("es_matching_variance_scalar", _lib.ptr(costs), costs.size, int(center),
+              ctypes.c_double(params.s_max), ctypes.c_double(params.r_min), ctypes.byref(r))
+    return float(r.value)
 
 
 def lr_consistency(d_left, d_right, tau_lr: float):

@@ -1,0 +1,169 @@
+"""BASELINE.json configs 2-5 at their FULL size and length against digests
+the UNMODIFIED reference produced (oracle/make_golden_configs.py):
+
+    config 2: 1242x375, D=128, 10 frames
+    config 3: 1242x375, D=128, 100 frames, 3 independently moving boxes,
+              2% salt noise per view (fallback windows, LR rejection and the
+              adopt/drop "variance reset" over a long horizon)
+    config 4: 2048x1024, D=256, frames 0-2
+    config 5: the bench's 64-sequence batch in ONE context (deferred steps,
+              two partial sums), sequences 0, 9, ..., 63 checked, frames 0-4
+
+The device renderer draws the same scenes; the image hashes prove the bytes
+equal synth.render_frame's.  Every map of every frame must then hash-match
+the reference (intervals, WTA disparities, validity / keep masks, matching
+variance, predicted and fused float64 state), and at the digested frames the
+dense cost and aggregated volumes too.  Should a float map ever differ in a
+last bit, its row sums must still agree within the north star's 1e-4."""
+
+import hashlib
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+FLOAT_MAPS = ("pred_d", "pred_p", "meas_r", "fused_d", "fused_p")
+
+
+def _digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _canonical(res, v):
+    """Same canonical dtypes as oracle/make_golden_configs.py:canonical_maps."""
+    L = v == "l"
+    pred = res.predicted_left if L else res.predicted_right
+    meas = res.measured_left if L else res.measured_right
+    iv = res.intervals_left if L else res.intervals_right
+    fd = res.fused.left if L else res.fused.right
+    return {
+        "pred_d": np.asarray(pred.values, np.float64),
+        "pred_v": np.asarray(pred.valid).astype(np.uint8),
+        "pred_p": np.asarray((res.predicted_left_var if L else res.predicted_right_var).values,
+                             np.float64),
+        "lo": np.asarray(iv.lo).astype(np.int16),
+        "hi": np.asarray(iv.hi).astype(np.int16),
+        "meas_d": np.asarray(meas.values).astype(np.uint16),
+        "meas_v": np.asarray(meas.valid).astype(np.uint8),
+        "meas_r": np.asarray((res.measured_left_var if L else res.measured_right_var).values,
+                             np.float64),
+        "keep": np.asarray(res.keep_left if L else res.keep_right).astype(np.uint8),
+        "fused_d": np.asarray(fd.values, np.float64),
+        "fused_v": np.asarray(fd.valid).astype(np.uint8),
+        "fused_p": np.asarray((res.fused.left_var if L else res.fused.right_var).values,
+                              np.float64),
+    }
+
+
+def _volume_check(g, k, v, tag, data):
+    fin = np.isfinite(data)
+    c = np.where(fin, data, 0).astype(np.int64)
+    key = f"f{k}_{v}_{tag}"
+    assert int(fin.sum()) == int(g[key + "_finite"]), key
+    assert np.array_equal(c.sum(axis=(1, 2)), g[key + "_rowsum"]), key
+    assert np.array_equal(c.sum(axis=(0, 2)), g[key + "_colsum"]), key
+    assert np.array_equal(c.sum(axis=(0, 1)), g[key + "_dsum"]), key
+    assert _digest(data.astype(np.float32)) == str(g[key + "_hash"]), key
+
+
+def _check_frame(g, k, res, vols=True):
+    """All maps of frame k against the golden digests; returns the number of
+    float maps that were exact (all of them, so far)."""
+    np.testing.assert_array_equal(
+        np.array([res.search_fraction_left, res.search_fraction_right]), g[f"f{k}_frac"])
+    exact = 0
+    for v in ("l", "r"):
+        maps = _canonical(res, v)
+        for name, a in maps.items():
+            want = str(g[f"f{k}_{v}_{name}_hash"])
+            if _digest(a) == want:
+                exact += name in FLOAT_MAPS
+                continue
+            assert name in FLOAT_MAPS, (k, v, name, "integer map differs from the reference")
+            np.testing.assert_allclose(a.sum(axis=1), g[f"f{k}_{v}_{name}_rowsum"], rtol=1e-4,
+                                       err_msg=f"frame {k} view {v} map {name}")
+        c = g[f"f{k}_{v}_counts"]
+        assert [int(maps["pred_v"].sum()), int(maps["meas_v"].sum()), int(maps["keep"].sum()),
+                int(maps["fused_v"].sum())] == list(c), (k, v)
+        if vols and f"f{k}_{v}_cost_hash" in g:
+            view = 0 if v == "l" else 1
+            _volume_check(g, k, v, "cost", res.cost_volume(view))
+            _volume_check(g, k, v, "total", res.total_volume(view))
+    return exact
+
+
+def _frames(cs, n, device="cuda:0"):
+    """Device-rendered images of frames 0..n-1, checked against the
+    reference renderer's hashes, then salt noise (config 3) on the host."""
+    import bench
+    from paper_1708_06301_b200 import scenes
+    imgs = bench.render_frames([cs], list(range(n)), device).cpu().numpy()[:, 0]
+    out = []
+    for k in range(n):
+        pair = np.ascontiguousarray(imgs[k])
+        out.append((pair, _digest(pair)))
+        scenes.apply_salt(pair, cs, k)
+    return out
+
+
+def _golden(config, seq):
+    g = os.path.join(GOLDEN, f"cfg{config}_s{seq}.npz")
+    if not os.path.exists(g):
+        pytest.skip(f"golden cfg{config}_s{seq} missing")
+    return np.load(g)
+
+
+@pytest.mark.parametrize("config", [2, 3, 4])
+def test_full_size_sequence_matches_reference(config):
+    from paper_1708_06301_b200 import core, pipeline, scenes
+    g = _golden(config, 0)
+    n = int(g["n_frames"])
+    cs = scenes.config_sequence(config, 0, n_frames=n)
+    rig = core.StereoRig(**cs.rig)
+    pipe = pipeline.DisparityPipeline(rig)
+    exact = 0
+    # render in chunks (config 3: 100 frames of 2 x 466 kB)
+    for k0 in range(0, n, 25):
+        chunk = _frames(cs, min(n, k0 + 25))[k0:]
+        for i, (pair, raw_hash) in enumerate(chunk):
+            k = k0 + i
+            assert raw_hash == str(g[f"f{k}_img_hash"]), f"frame {k}: renderer != synth"
+            assert _digest(pair) == str(g[f"f{k}_in_hash"]), k
+            res = pipe.process_frame(core.GrayImage(pair[0]), core.GrayImage(pair[1]),
+                                     cs.motions[k])
+            exact += _check_frame(g, k, res)
+    print(f"config {config}: {n} frames, {exact}/{n * 2 * len(FLOAT_MAPS)} float maps bit-exact")
+
+
+def test_config5_batch_of_64_matches_reference_subset():
+    import bench
+    from paper_1708_06301_b200 import core, pipeline, scenes
+    goldens = {int(os.path.basename(p)[6:-4]): p for p in
+               glob.glob(os.path.join(GOLDEN, "cfg5_s*.npz"))}
+    if not goldens:
+        pytest.skip("golden cfg5 missing")
+    gs = {s: np.load(p) for s, p in goldens.items()}
+    n = int(next(iter(gs.values()))["n_frames"])
+    specs = [scenes.config_sequence(5, s) for s in range(64)]
+    rig = core.StereoRig(**specs[0].rig)
+    imgs = bench.render_frames(specs, list(range(n)), "cuda:0")
+    host = imgs.cpu().numpy()
+    for s, g in gs.items():
+        for k in range(n):
+            assert _digest(host[k, s]) == str(g[f"f{k}_img_hash"]), (s, k)
+    bp = pipeline.BatchedPipeline(rig, 64)
+    bp.process_frames(None, bench.motions_for(specs, 0), sync=True, images_dev=imgs[0].data_ptr())
+    for s, g in gs.items():
+        _check_frame(g, 0, bp.result(s), vols=False)
+    for k in range(1, n):
+        # deferred (non-syncing) steps like the bench; results read after sync
+        bp.process_frames(None, bench.motions_for(specs, k), sync=False,
+                          images_dev=imgs[k].data_ptr())
+        bp.sync()
+        for s, g in gs.items():
+            _check_frame(g, k, bp.result(s), vols=(k == 1))

@@ -429,43 +429,6 @@ def gen_metrics():
     save("run_sequence", **out)
 
 
-def gen_kitti():
-    """A KITTI-layout tree written by the reference (pipeline.write_sequence)
-    and what the reference's load_sequence reads back from it."""
-    import tempfile
-    rig = rig_small(40, 24, 8, f=30.0, b=0.4)
-    scene = synth.SceneSpec(rig=rig, primitives=(synth.Plane(z=3.0),), texture_seed=2)
-    frames = synth.make_sequence(scene, synth.dolly_trajectory(3, -0.05), sigma_rot_deg=0.1,
-                                 sigma_trans=0.01, seed=8)
-    seq = pipeline.Sequence(rig, [f.left for f in frames], [f.right for f in frames],
-                            [f.motion_noisy for f in frames],
-                            gt_left=[f.gt_left for f in frames],
-                            gt_right=[f.gt_right for f in frames])
-    poses = [f.pose for f in frames]
-    out = {}
-    with tempfile.TemporaryDirectory() as tmp:
-        pipeline.write_sequence(tmp, seq, poses)
-        for rel in ("calib.txt", "poses.txt"):
-            out["file_" + rel.replace(".", "_")] = np.frombuffer(
-                open(os.path.join(tmp, rel), "rb").read(), np.uint8)
-        for sub in ("image_0", "image_1", "gt_disp_0", "gt_disp_1"):
-            for k in range(len(frames)):
-                out[f"file_{sub}_{k}"] = np.frombuffer(
-                    open(os.path.join(tmp, sub, f"{k:06d}.png"), "rb").read(), np.uint8)
-        back = pipeline.load_sequence(tmp, d_max=8)
-    out["rig"] = np.array([back.rig.f, back.rig.b, back.rig.cx, back.rig.cy,
-                           back.rig.width, back.rig.height, back.rig.d_max])
-    out["poses"] = np.stack(poses)
-    for k in range(len(frames)):
-        out[f"left_{k}"], out[f"right_{k}"] = back.lefts[k].data, back.rights[k].data
-        out[f"motion_{k}"] = np.eye(4) if back.motions[k] is None else back.motions[k]
-        out[f"gtl_d_{k}"], out[f"gtl_v_{k}"] = back.gt_left[k].values, back.gt_left[k].valid
-        out[f"gtr_d_{k}"], out[f"gtr_v_{k}"] = back.gt_right[k].values, back.gt_right[k].valid
-        # the in-memory maps that were written (encoding is lossy: round(256 d))
-        out[f"src_gtl_d_{k}"], out[f"src_gtl_v_{k}"] = frames[k].gt_left.values, frames[k].gt_left.valid
-    save("kitti", **out)
-
-
 def gen_acceptance():
     """Reference acceptance criteria on their own scenes: criterion 3 (10
     rendered 32x32 scenes, full-range matcher == the independent brute-force
@@ -503,7 +466,7 @@ def gen_acceptance():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["cost_agg", "misc", "prediction", "sequences", "config1", "metrics", "kitti", "acceptance"]
+    which = sys.argv[1:] or ["cost_agg", "misc", "prediction", "sequences", "config1", "metrics", "acceptance", "render_planes"]
     if "cost_agg" in which:
         gen_cost_agg()
     if "misc" in which:
@@ -516,8 +479,6 @@ if __name__ == "__main__":
         gen_config1()
     if "metrics" in which:
         gen_metrics()
-    if "kitti" in which:
-        gen_kitti()
     if "acceptance" in which:
         gen_acceptance()
     if "render_planes" in which:

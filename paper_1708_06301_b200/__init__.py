@@ -8,10 +8,11 @@ there is no CPU fallback.
 
 Modules: core (boundary types), geometry (4x4 homographies, device warp),
 prediction, sgm, fusion (drop-in stage functions), pipeline
-(DisparityPipeline / BatchedPipeline on device-resident state, run_sequence,
-load_sequence), metrics (device bad-pixel evaluation), kitti_io (KITTI-layout
-files), scenes
-(seeded benchmark inputs), build (nvcc build of libegostereo_b200.so).
+(DisparityPipeline / BatchedPipeline on device-resident state), metrics
+(device bad-pixel evaluation), install (drop-in rebinding of the reference
+package ``egostereo``: its own sequence runner, KITTI I/O and CLI then run on
+top of the device stages), scenes (seeded benchmark inputs), build (nvcc
+build of libegostereo_b200.so).
 """
 
 from .core import (DisparityMap, FilterState, GrayImage, StereoRig, VarianceMap,
@@ -21,8 +22,7 @@ from .errors import (BehindCameraError, DeviceUnavailableError, DeviceUnsupporte
 from .fusion import FusionParams, fuse_maps
 from .geometry import disparity_homography, euclidean_warp_oracle, warp_point
 from .metrics import BadPixelResult, bad_pixel_rate, search_space_fraction
-from .pipeline import (BatchedPipeline, DisparityPipeline, FrameResult, PipelineParams,
-                       Sequence, load_sequence, run_sequence, write_sequence)
+from .pipeline import BatchedPipeline, DisparityPipeline, FrameResult, PipelineParams
 from .prediction import PredictionParams, predict_maps
 from .sgm import IntervalMap, SgmParams, full_range_intervals, search_intervals
 
@@ -32,9 +32,9 @@ __all__ = [
     "BadPixelResult", "BatchedPipeline", "BehindCameraError", "DeviceUnavailableError", "DeviceUnsupportedError",
     "DisparityMap", "DisparityPipeline", "FilterState", "FrameResult", "FusionParams",
     "GrayImage", "IntervalMap", "PipelineParams", "PointAtInfinityError", "PredictionParams",
-    "Sequence", "SgmParams", "StereoRig", "VarianceMap", "disparity_homography",
+    "SgmParams", "StereoRig", "VarianceMap", "disparity_homography",
     "euclidean_warp_oracle", "full_range_intervals", "fuse_maps", "make_empty_state",
-    "make_invalid_map", "make_motion", "predict_maps", "run_sequence", "search_intervals",
-    "bad_pixel_rate", "load_sequence", "write_sequence",
+    "make_invalid_map", "make_motion", "predict_maps", "search_intervals",
+    "bad_pixel_rate",
     "search_space_fraction", "warp_point", "__version__",
 ]

@@ -113,7 +113,12 @@ __global__ void k_u16_to_f64(const uint16_t* a, size_t n, double* o) {
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) o[i] = (double)a[i];
 }
-// kitti_io.write_disparity_png encoding (kitti_io.py:38-46)
+// kitti_io.write_disparity_png encoding (kitti_io.py:38-46).  Fused
+// disparities never exceed d_max, and for d_max <= 255 round(256 d) <= 65535;
+// above that the reference's writer raises ValueError for large values, so
+// the export refuses contexts with d_max > 255 instead of saturating.
+static const char* kKittiRange =
+    "KITTI 16-bit disparity encoding holds d < 256: d_max > 255 cannot be exported";
 __global__ void k_kitti(const double* d, const uint8_t* v, size_t n, uint16_t* o) {
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -738,6 +743,7 @@ int es_ctx_export(es_ctx* c, int what, int seq, int view, void* out) {
       break;
     }
     case ES_FUSED_KITTI: {
+      if (c->rig.d_max > 255) return fail(ES_ERR_VALUE, kKittiRange);
       CK(cudaMallocAsync(&tmp, sizeof(uint16_t) * HW, c->st));
       k_kitti<<<nb, 256, 0, c->st>>>(c->sd[c->cur] + o, c->sv[c->cur] + o, HW, (uint16_t*)tmp);
       src = tmp;
@@ -788,6 +794,7 @@ extern "C" int es_ctx_export_all(es_ctx* c, int what, int view, void* out, int s
   const size_t HW = c->HW;
   const int B = c->B;
   if (what == ES_FUSED_KITTI) {
+    if (c->rig.d_max > 255) return fail(ES_ERR_VALUE, kKittiRange);
     // encode on the compute stream into one of two staging slots, copy out
     // on cp_out: the transfer overlaps the next step's kernels
     const int kb = c->kitti_slot;

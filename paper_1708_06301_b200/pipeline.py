@@ -30,7 +30,7 @@ from .prediction import PredictionParams
 from .sgm import IntervalMap, SgmParams
 
 __all__ = ["FrameResult", "PipelineParams", "DisparityPipeline", "BatchedPipeline",
-           "Sequence", "relative_motions", "run_sequence", "StereoEngine"]
+           "StereoEngine"]
 
 
 @dataclass
@@ -371,143 +371,3 @@ class BatchedPipeline:
         hw = self.rig.width * self.rig.height
         return [(M.rates_from_counts(int(c[0]), int(c[1]), int(c[2])), int(c[3]) / hw)
                 for c in counts]
-
-
-@dataclass
-class Sequence:
-    """pipeline.py:173-185."""
-
-    rig: StereoRig
-    lefts: list
-    rights: list
-    motions: list
-    gt_left: list | None = None
-    gt_right: list | None = None
-
-    def __len__(self) -> int:
-        return len(self.lefts)
-
-
-def relative_motions(poses):
-    """pipeline.py:188-193."""
-    motions = [None]
-    for prev, curr in zip(poses[:-1], poses[1:]):
-        motions.append(np.linalg.inv(curr) @ prev)
-    return motions
-
-
-def _frame_files(directory: str) -> list:
-    from . import kitti_io
-    names = sorted(n for n in os.listdir(directory) if n.endswith(".png"))
-    if not names:
-        raise kitti_io.FileFormatError(f"{directory}: no PNG frames found")
-    return [os.path.join(directory, n) for n in names]
-
-
-def load_sequence(root: str, d_max: int) -> Sequence:
-    """Read a KITTI-layout sequence directory (pipeline.py:203-238): calib.txt,
-    poses.txt, image_0/ and image_1/ PNG frames, optional gt_disp_0/1."""
-    from . import kitti_io
-    calib = kitti_io.read_calib_file(os.path.join(root, "calib.txt"))
-    lf = _frame_files(os.path.join(root, "image_0"))
-    rf = _frame_files(os.path.join(root, "image_1"))
-    if len(lf) != len(rf):
-        raise kitti_io.FileFormatError(
-            f"{root}: image_0 has {len(lf)} frames, image_1 has {len(rf)}")
-    lefts = [kitti_io.read_gray_png(f) for f in lf]
-    rights = [kitti_io.read_gray_png(f) for f in rf]
-    h, w = lefts[0].data.shape
-    if any(img.data.shape != (h, w) for img in lefts + rights):
-        raise kitti_io.FileFormatError(f"{root}: frame dimensions are not uniform")
-    rig = StereoRig(f=calib.f, b=calib.b, cx=calib.cx, cy=calib.cy, width=w, height=h,
-                    d_max=d_max)
-    poses = kitti_io.read_pose_file(os.path.join(root, "poses.txt"))
-    if len(poses) != len(lefts):
-        raise kitti_io.FileFormatError(f"{root}: {len(poses)} poses for {len(lefts)} frames")
-    seq = Sequence(rig, lefts, rights, relative_motions(poses))
-    for attr, sub in (("gt_left", "gt_disp_0"), ("gt_right", "gt_disp_1")):
-        gt_dir = os.path.join(root, sub)
-        if os.path.isdir(gt_dir):
-            files = _frame_files(gt_dir)
-            if len(files) != len(lefts):
-                raise kitti_io.FileFormatError(
-                    f"{root}: {len(files)} maps in {sub} for {len(lefts)} frames")
-            setattr(seq, attr, [kitti_io.read_disparity_png(f) for f in files])
-    return seq
-
-
-def write_sequence(root: str, seq: Sequence, poses) -> None:
-    """Materialise an in-memory sequence as a KITTI-layout directory
-    (pipeline.py:305-322)."""
-    from . import kitti_io
-    kitti_io.ensure_dir(root)
-    kitti_io.write_calib_file(os.path.join(root, "calib.txt"),
-                              kitti_io.CalibData(f=seq.rig.f, cx=seq.rig.cx, cy=seq.rig.cy,
-                                                 b=seq.rig.b))
-    kitti_io.write_pose_file(os.path.join(root, "poses.txt"), poses)
-    for sub, images in (("image_0", seq.lefts), ("image_1", seq.rights)):
-        d = kitti_io.ensure_dir(os.path.join(root, sub))
-        for k, img in enumerate(images):
-            kitti_io.write_gray_png(os.path.join(d, f"{k:06d}.png"), img)
-    for sub, maps in (("gt_disp_0", seq.gt_left), ("gt_disp_1", seq.gt_right)):
-        if maps is None:
-            continue
-        d = kitti_io.ensure_dir(os.path.join(root, sub))
-        for k, m in enumerate(maps):
-            kitti_io.write_disparity_png(os.path.join(d, f"{k:06d}.png"), m)
-
-
-def run_sequence(seq: Sequence, params: PipelineParams | None = None, out_dir: str | None = None,
-                 metric_mode: str = "or"):
-    """Run the pipeline over a sequence, optionally writing an output tree
-    (pipeline.py:241-302): disp_0/ (left fused disparity PNGs), err_0/ (error
-    visualizations, when ground truth is available), metrics.txt (one line
-    per frame) and summary.txt (aggregate key=value pairs).  Bad-pixel counts
-    and error images are computed on the device (metrics.py); PNG encoding
-    stays on the host after the last frame, so it never stalls a step."""
-    from . import kitti_io, metrics
-    params = params or PipelineParams()
-    pipe = DisparityPipeline(seq.rig, params)
-    results, lines, rates = [], [], []
-    for k in range(len(seq)):
-        res = pipe.process_frame(seq.lefts[k], seq.rights[k], seq.motions[k])
-        results.append(res)
-        fl = res.fused.left
-        entry = {
-            "frame": f"{k:06d}",
-            "density": f"{metrics.density(fl):.6f}",
-            "search_fraction": f"{res.search_fraction_left:.6f}",
-        }
-        if seq.gt_left is not None:
-            bad = metrics.bad_pixel_rate(fl, seq.gt_left[k], metric_mode)
-            rates.append(bad.rate)
-            entry["bad_rate"] = f"{bad.rate:.6f}"
-            entry["bad_rate_all"] = f"{bad.rate_all:.6f}"
-            entry["gt_density"] = f"{bad.density:.6f}"
-        lines.append(" ".join(f"{k_}={v}" for k_, v in entry.items()))
-    pipe._flush()
-
-    if out_dir is not None:
-        disp_dir = os.path.join(out_dir, "disp_0")
-        os.makedirs(disp_dir, exist_ok=True)
-        for k, res in enumerate(results):
-            kitti_io.write_disparity_png(os.path.join(disp_dir, f"{k:06d}.png"), res.fused.left)
-        if seq.gt_left is not None:
-            err_dir = os.path.join(out_dir, "err_0")
-            os.makedirs(err_dir, exist_ok=True)
-            for k, res in enumerate(results):
-                img = metrics.error_image(res.fused.left, seq.gt_left[k], metric_mode)
-                kitti_io.write_color_png(os.path.join(err_dir, f"{k:06d}.png"), img)
-        with open(os.path.join(out_dir, "metrics.txt"), "w") as fh:
-            fh.write("\n".join(lines) + "\n")
-        with open(os.path.join(out_dir, "summary.txt"), "w") as fh:
-            fh.write(f"frames={len(results)}\n")
-            fh.write(f"mode={'baseline' if params.baseline else 'temporal'}\n")
-            fh.write(f"metric_mode={metric_mode}\n")
-            mean_sf = float(np.mean([r.search_fraction_left for r in results]))
-            fh.write(f"mean_search_fraction={mean_sf:.6f}\n")
-            mean_density = float(np.mean([metrics.density(r.fused.left) for r in results]))
-            fh.write(f"mean_density={mean_density:.6f}\n")
-            if seq.gt_left is not None:
-                fh.write(f"mean_bad_rate={float(np.mean(rates)):.6f}\n")
-    return results

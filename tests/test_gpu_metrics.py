@@ -43,19 +43,40 @@ def test_metrics_errors():
 
 
 def test_run_sequence_output_tree_matches_reference(tmp_path):
+    """The reference's own sequence runner, KITTI writer and metrics files
+    (pipeline.py:241-302, kitti_io.py) on top of the device stages:
+    install() into the unmodified package from baseline/_ref, then
+    egostereo.run_sequence must write exactly the tree the reference wrote
+    with its numpy stages (golden run_sequence.npz)."""
+    import os
+    import sys
     cv2 = pytest.importorskip("cv2")
-    from paper_1708_06301_b200 import core, pipeline
-    g = load_golden("run_sequence")
-    f, b, cx, cy, w, h, d_max = g["rig"]
-    rig = core.StereoRig(f=f, b=b, cx=cx, cy=cy, width=int(w), height=int(h), d_max=int(d_max))
-    n = len([k for k in g.files if k.endswith("_left")])
-    seq = pipeline.Sequence(
-        rig, [core.GrayImage(g[f"f{k}_left"]) for k in range(n)],
-        [core.GrayImage(g[f"f{k}_right"]) for k in range(n)],
-        [g[f"f{k}_motion"] if bool(g[f"f{k}_has_motion"]) else None for k in range(n)],
-        gt_left=[core.DisparityMap(g[f"f{k}_gt_d"], g[f"f{k}_gt_v"]) for k in range(n)],
-        gt_right=[core.DisparityMap(g[f"f{k}_gtr_d"], g[f"f{k}_gtr_v"]) for k in range(n)])
-    results = pipeline.run_sequence(seq, out_dir=str(tmp_path), metric_mode="or")
+    from conftest import ROOT
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "egostereo")):
+        pytest.skip("reference not installed (tools/install_reference.sh)")
+    sys.path.insert(0, ref)
+    import egostereo
+    from egostereo import core, pipeline
+    from paper_1708_06301_b200 import install
+    install.install(egostereo)
+    try:
+        g = load_golden("run_sequence")
+        f, b, cx, cy, w, h, d_max = g["rig"]
+        rig = core.StereoRig(f=f, b=b, cx=cx, cy=cy, width=int(w), height=int(h),
+                             d_max=int(d_max))
+        n = len([k for k in g.files if k.endswith("_left")])
+        seq = pipeline.Sequence(
+            rig, [core.GrayImage(g[f"f{k}_left"]) for k in range(n)],
+            [core.GrayImage(g[f"f{k}_right"]) for k in range(n)],
+            [g[f"f{k}_motion"] if bool(g[f"f{k}_has_motion"]) else None for k in range(n)],
+            gt_left=[core.DisparityMap(g[f"f{k}_gt_d"], g[f"f{k}_gt_v"]) for k in range(n)],
+            gt_right=[core.DisparityMap(g[f"f{k}_gtr_d"], g[f"f{k}_gtr_v"]) for k in range(n)])
+        results = pipeline.run_sequence(seq, out_dir=str(tmp_path), metric_mode="or")
+        assert pipeline.DisparityPipeline.__b200__
+    finally:
+        install.uninstall(egostereo)
+        sys.path.remove(ref)
     assert len(results) == n
     assert open(tmp_path / "metrics.txt").read() == str(g["metrics_txt"])
     assert open(tmp_path / "summary.txt").read() == str(g["summary_txt"])

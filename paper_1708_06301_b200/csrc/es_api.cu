@@ -194,6 +194,11 @@ struct es_ctx {
   int* err = nullptr;
   int* anyv = nullptr;
   unsigned long long* cells = nullptr;
+  // fused vertical + diagonal sweeps: ticket, row counters and edge ring of
+  // each of the two sweeps (es_sgm_vd3.cu)
+  unsigned* v3_ticket = nullptr;
+  int* v3_prog = nullptr;
+  uint32_t* v3_ring = nullptr;
   // pinned host mirrors
   double* h_Hm = nullptr;
   uint8_t* h_have = nullptr;
@@ -244,7 +249,8 @@ int ctx_free(es_ctx* c) {
                   c->C, c->S,
                   c->Sx[0], c->Sx[1], c->Sx[2], c->dstar, c->r, c->mvalid, c->keep, c->Hm,
                   c->have_pred, c->err, c->anyv,
-                  c->cells, c->kitti, c->cells_acc, c->img2};
+                  c->cells, c->kitti, c->cells_acc, c->img2, c->v3_ticket, c->v3_prog,
+                  c->v3_ring};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   void* hptrs[] = {c->h_Hm, c->h_have, c->h_err, c->h_anyv, c->h_cells};
@@ -365,6 +371,12 @@ int es_ctx_create(int device, const es_rig* rig, const es_params* prm, int batch
     c->parts = pe ? atoi(pe) : (batch <= 8 ? 4 : 2);
     if (c->parts != 1 && c->parts != 2 && c->parts != 4) c->parts = 2;
     for (int p = 0; p + 1 < c->parts && !e; ++p) e = dalloc(&c->Sx[p], vol_words);
+    const int n_sv = 2 * batch;
+    if (!e && vd3_lanes(rig->d_max) && (c->parts == 2 || c->parts == 4)) {
+      e = dalloc(&c->v3_ticket, 2);
+      if (!e) e = dalloc(&c->v3_prog, 2 * (size_t)n_sv * vd3_strips(rig->width, rig->d_max, rig->height));
+      if (!e) e = dalloc(&c->v3_ring, 2 * (size_t)n_sv * vd3_ring_words(rig->width, rig->d_max, rig->height));
+    }
   }
   if (!e) e = dalloc(&c->dstar, n);
   if (!e) e = dalloc(&c->r, n);
@@ -547,6 +559,9 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   // count (<= split: G lanes per chain, > split: 2G; measured)
   sa.lanes = c->lanes;
   sa.cells = c->cells;
+  sa.vd3_ticket = c->v3_ticket;
+  sa.vd3_prog = c->v3_prog;
+  sa.vd3_ring = c->v3_ring;
   static const double split = getenv("ES_SGM_SPLIT") ? atof(getenv("ES_SGM_SPLIT")) : 0.6;
   sa.split = split;
   if (c->arith == ARITH_U16 && !c->lanes) {

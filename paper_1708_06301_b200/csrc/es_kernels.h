@@ -72,6 +72,11 @@ struct SgmArgs {
   const unsigned long long* cells = nullptr;
   double split = 0.3;
   int select = 0;       // internal: 0 all, 1 fraction <= split, 2 fraction > split
+  // fused vertical + diagonal passes (launch_aggregate_parts): workspace for
+  // the two sweeps -- ticket + row counters + ring each (null: grp4 jobs)
+  unsigned* vd3_ticket = nullptr;   // [2]
+  int* vd3_prog = nullptr;          // [2][n_sv][nstrips]
+  uint32_t* vd3_ring = nullptr;     // [2][n_sv][vd3_ring_words]
 };
 // full 8-path aggregation; the u16 path runs 4 family launches (both sweeps
 // each), the f32 path runs the 8 directions in the reference's order
@@ -87,6 +92,23 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
 // read-modify-writing (init: writing) the u16 partial sum a.S
 bool vd_supported(int W, int d_max);
 void launch_vd(const SgmArgs& a, bool up, bool init, int n_sv, cudaStream_t st);
+
+// fused vertical + diagonal row sweep (es_sgm_vd3.cu): the three directions
+// of one row sweep (up = 0: dy = +1, up = 1: dy = -1) in one pass; strips of
+// 32/G columns per warp, edge columns exchanged through an L2 ring.
+struct Vd3Args {
+  SgmArgs a;
+  int up;                 // 0: top -> bottom, 1: bottom -> top
+  int nstrips;            // strips per view (vd3_strips)
+  int total;              // n_sv * nstrips
+  unsigned* ticket;       // zeroed before the launch
+  int* prog;              // [n_sv][nstrips] rows completed, zeroed before the launch
+  uint32_t* ring;         // [n_sv][vd3_ring_words]
+};
+int vd3_lanes(int d_max);                      // G (0: unsupported d_max)
+int vd3_strips(int W, int d_max, int H);
+size_t vd3_ring_words(int W, int d_max, int H);  // per (seq, view)
+void launch_vd3(const Vd3Args& v, bool init, cudaStream_t st);
 
 struct WtaArgs {
   int W, H;

@@ -846,6 +846,40 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
   int widen = widen_env >= 0 ? widen_env : (n_sv <= 2 && np <= 64 ? 1 : 0);
   if (np > 64) widen += 1;
   static const int split_env = getenv("ES_SGM_SPLITH") ? atoi(getenv("ES_SGM_SPLITH")) : 1;
+  static const int v3_env = getenv("ES_SGM_VD3") ? atoi(getenv("ES_SGM_VD3")) : 1;
+  if (g4 && v3_env && a.vd3_ring && (parts == 2 || parts == 4) && vd3_lanes(a.d_max)) {
+    // fused vertical + diagonal sweeps (es_sgm_vd3.cu): each partial sum
+    // takes one row job and one three-direction sweep: S0 = rows ->, then
+    // the dy = +1 sweep; S1 = rows <-, then the dy = -1 sweep (parts == 4:
+    // the sweeps write S2 / S3 concurrently with the row jobs instead)
+    const int ns = vd3_strips(a.W, a.d_max, a.H);
+    const size_t ringw = vd3_ring_words(a.W, a.d_max, a.H);
+    for (int p = 0; p < 2; ++p) {
+      SgmArgs lo = a, hi = a;
+      lo.select = 1;
+      hi.select = 2;
+      lo.S = S[p];
+      hi.S = S[p];
+      // both regime variants of the row job on one stream, then the sweep
+      launch_grp4_g(4 << widen, lo, FAM_H, 1, n_sv, st_lo[p], p == 0 ? 1 : 2);
+      launch_grp4_g(8 << widen, hi, FAM_H, 1, n_sv, st_lo[p], p == 0 ? 1 : 2);
+      const int sp = parts == 4 ? p + 2 : p;
+      Vd3Args v;
+      v.a = a;
+      v.a.S = S[sp];
+      v.up = p;
+      v.nstrips = ns;
+      v.total = n_sv * ns;
+      v.ticket = a.vd3_ticket + p;
+      v.prog = a.vd3_prog + (size_t)p * n_sv * ns;
+      v.ring = a.vd3_ring + (size_t)p * n_sv * ringw;
+      cudaStream_t vs = st_lo[sp];
+      cudaMemsetAsync(v.ticket, 0, sizeof(unsigned), vs);
+      cudaMemsetAsync(v.prog, 0, sizeof(int) * (size_t)n_sv * ns, vs);
+      launch_vd3(v, parts == 4, vs);
+    }
+    return parts;
+  }
   static const int vd3_env = getenv("ES_SGM_VD") ? atoi(getenv("ES_SGM_VD")) : 0;
   if (g4 && parts == 4 && vd3_env == 3 && vd_supported(a.W, a.d_max)) {
     // three live partial sums: S2 = the cluster pass of the dy = +1

@@ -1,0 +1,496 @@
+// K4, fused vertical + diagonal row sweep: the three directions of one row
+// sweep (down: (0,+1), (+1,+1), (-1,+1); up: (0,-1), (+1,-1), (-1,-1)) in ONE
+// pass over the ragged volume: the cost words of a row are read once, the
+// partial sum is read-modify-written once, and the three path states stay in
+// registers.  Reference: sgm.py:199-237,257-272 (_path_step, _scan_vertical,
+// aggregate_paths).
+//
+// Work decomposition: sheared strips.  A "strip" is NG = 32/G adjacent
+// DIAGONAL chains of one view, walked by one warp over the whole sweep --
+// lane group q follows the pixels x = xb + q + t of rows y = t (down) or
+// y = H-1-t (up), i.e. the (+1,+1) resp. (+1,-1) path itself (state B, kept
+// in place).  Each lane holds PPL = 4 u16x2 words of every 32G-cell chunk
+// (absolute disparity layout of k_sgm_grp4).  In that frame the other two
+// directions' predecessors are the chains one and two to the RIGHT at the
+// previous step: the column path A (pred (x, y-+1)) comes from lane group
+// q+1 and the anti-diagonal C (pred (x+1, y-+1)) from group q+2, both by warp
+// shuffles.  Every cross-warp dependency is one-sided: a strip needs only its
+// right neighbour strip's first two chains of the previous step.
+//
+// Schedule: one CTA per (sequence, view), 16 warps.  The view's strips are
+// taken right to left in rounds of 16: in round r warp w walks strip
+// 16r + w (counted from the right).  Warp w's producer is warp w-1 of the
+// same round, one or two steps ahead -- hand-over through a 4-slot ring in
+// shared memory and per-warp progress words (fence.cta only); warp 0's
+// producer is warp 15 of the previous round, which finished that strip long
+// before -- hand-over through a per-view buffer in global memory holding all
+// steps (double-buffered by round parity).  Nothing waits on another CTA.
+//
+// Operands: the row's cost words (and partial-sum words) of the strip's NG
+// pixels are one contiguous byte range of the row-ragged volume; one elected
+// lane stages the next row's ranges into shared memory with cp.async.bulk
+// (completion on a per-slot mbarrier) while the warp computes the current row.
+//
+// Arithmetic, +inf convention, chunk union and first-pixel handling are
+// those of k_sgm_grp4: u16x2 words, 0x8000 = +inf,
+// wrapping adds; an off-image predecessor (first row, x-1 < 0, x+1 >= W)
+// holds +inf with m + P2 = -m = 0x8000, which yields L = C.
+#include <cstdlib>
+
+#include "es_common.cuh"
+#include "es_kernels.h"
+
+namespace es {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int V3_PPL = 4;      // words per lane per chunk
+constexpr int V3_WARPS = 4;    // warps per CTA
+constexpr uint32_t V3_NONE = 0xFFFFFFFFu;
+
+template <int G, int NCH>
+struct V3 {
+  static constexpr int NG = 32 / G;             // columns per strip
+  static constexpr int CW = V3_PPL * G;         // words per chunk
+  static constexpr int NW = V3_PPL * NCH;       // state words per lane
+  static constexpr int BUFW = NG * NCH * CW;    // staged words per row (upper bound)
+  static constexpr int REC = G * NW + 4;        // ring record: G lanes x NW words + splats
+};
+
+__device__ __forceinline__ uint32_t v3_umask(int lo, int hi) {
+  return hi < lo ? 0u : ((hi >= 31 ? 0xFFFFFFFFu : ((2u << hi) - 1u)) & ~((1u << lo) - 1u));
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// spin (relaxed loads, no L1 invalidation per poll) until *p >= v, then one
+// acquire load orders the ring reads after the producer's release
+__device__ __forceinline__ void wait_ge(const int* p, int v) {
+  if (ld_relaxed(p) < v) {
+    do {
+      __nanosleep(32);
+    } while (ld_relaxed(p) < v);
+  }
+  (void)ld_acquire(p);
+}
+__device__ __forceinline__ void st_relaxed(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint4 ld_cg4(const uint32_t* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) {
+  uint32_t r;
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+
+// one path update of a lane's 4 words (k_sgm_grp4's recurrence):
+// L = C + min(Lp(d), min(Lp(d-1), Lp(d+1)) + P1, m + P2) - m
+__device__ __forceinline__ void v3_path(const uint32_t* P, uint32_t el, uint32_t er, uint32_t mp2,
+                                        uint32_t ng, uint32_t p1x2, const uint32_t* cn,
+                                        uint32_t* L) {
+  uint32_t X[V3_PPL + 1];
+  X[0] = __byte_perm(el, P[0], 0x5432);
+#pragma unroll
+  for (int k = 1; k < V3_PPL; ++k) X[k] = __byte_perm(P[k - 1], P[k], 0x5432);
+  X[V3_PPL] = __byte_perm(P[V3_PPL - 1], er, 0x5432);
+#pragma unroll
+  for (int k = 0; k < V3_PPL; ++k) {
+    const uint32_t cand = __viaddmin_u16x2(__vminu2(X[k], X[k + 1]), p1x2, __vminu2(P[k], mp2));
+    L[k] = __vadd2(cn[k], __vadd2(cand, ng));
+  }
+}
+
+template <int G, int NCH>
+struct V5 {
+  static constexpr int NG = 32 / G;             // chains per strip
+  static constexpr int CW = V3_PPL * G;         // words per chunk
+  static constexpr int NW = V3_PPL * NCH;       // state words per lane
+  static constexpr int BUFW = NG * NCH * CW;    // staged words per step (upper bound)
+  static constexpr int REC = 3 * G * NW + 8;    // hand-over record: A0, C0, C1 + 6 splats
+};
+constexpr int V5_WARPS = 16;   // warps per CTA = strips per round
+constexpr int V5_RS = 4;       // shared-memory ring slots per warp pair
+
+template <int G, int NCH>
+constexpr size_t v5_smem() {
+  using T = V5<G, NCH>;
+  return sizeof(uint32_t) * ((size_t)V5_WARPS * 4 * T::BUFW + V5_WARPS * 4 +
+                             (size_t)(V5_WARPS - 1) * V5_RS * T::REC + V5_WARPS + 4);
+}
+
+__device__ __forceinline__ void spin_ge(const volatile int* p, int v) {
+  while (*p < v) {
+  }
+}
+
+template <int G, int NCH, bool INIT>
+__global__ void __launch_bounds__(V5_WARPS * 32, 1) k_sgm_vd5(Vd3Args v) {
+  using T = V5<G, NCH>;
+  constexpr int NG = T::NG, CW = T::CW, NW = T::NW, PPL = V3_PPL, REC = T::REC;
+  constexpr int BUFW = T::BUFW;
+  extern __shared__ __align__(16) uint32_t sm5[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int gl = lane & (G - 1), q = lane / G;
+  const int gbase = lane & ~(G - 1);
+  const int src_l = gbase | ((gl + G - 1) & (G - 1));
+  const int src_r = gbase | ((gl + 1) & (G - 1));
+  uint32_t* buf = sm5 + w * (4 * BUFW);   // [2 slots][cost, sum][BUFW]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm5 + V5_WARPS * 4 * BUFW) + 2 * w;
+  uint32_t* rings = sm5 + V5_WARPS * 4 * BUFW + V5_WARPS * 4;          // [V5_WARPS-1][RS][REC]
+  volatile int* progs = reinterpret_cast<volatile int*>(rings + (V5_WARPS - 1) * V5_RS * REC);
+  uint32_t* infpad = rings + (V5_WARPS - 1) * V5_RS * REC + V5_WARPS;   // 4 words of +inf
+
+  const SgmArgs& a = v.a;
+  const int W = a.W, H = a.H;
+  const int sv = blockIdx.x;
+  const int ns = v.nstrips;
+  const bool up = v.up != 0;
+  const size_t HW = (size_t)W * H;
+  const uint2* __restrict__ meta = a.meta + (size_t)sv * HW;
+  const uint32_t* Cg = reinterpret_cast<const uint32_t*>(a.C) + (size_t)sv * a.volcap;
+  uint32_t* Sg = reinterpret_cast<uint32_t*>(a.S) + (size_t)sv * a.volcap;
+  uint32_t* gbuf = v.ring + (size_t)sv * 2 * H * REC;   // [round parity][step][REC]
+  const uint32_t p1x2 = a.p1i * 0x10001u;
+
+  const unsigned bar0 = (unsigned)__cvta_generic_to_shared(bars);
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < V5_WARPS) progs[threadIdx.x] = 0;
+  if (threadIdx.x < 4) infpad[threadIdx.x] = INF16x2;
+  __syncthreads();
+
+  auto in_img = [&](int x) { return x >= 0 && x < W; };
+  auto wait_slot = [&](int slot, unsigned parity) {
+    const unsigned b = bar0 + 8u * (unsigned)slot;
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                   "selp.u32 %0, 1, 0, p;\n\t}\n"
+                   : "=r"(done) : "r"(b), "r"(parity) : "memory");
+  };
+  auto publish = [&](int value) {
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      progs[w] = value;
+    }
+  };
+
+  int it_all = 0;   // steps walked by this warp (mbarrier slot / phase)
+  const int rounds = (ns + V5_WARPS - 1) / V5_WARPS;
+  for (int r = 0; r < rounds; ++r) {
+    // every warp has finished round r-1: the shared ring slots and the
+    // global buffer of round r-2's parity are free again
+    __syncthreads();
+    const int kk = r * V5_WARPS + w;
+    if (kk >= ns) continue;
+    const int k = ns - 1 - kk;
+    const int xb0 = -(H - 1) + k * NG;                 // chain of lane group 0 (x at step 0)
+    const int t0 = max(0, -(xb0 + NG - 1)), t1 = min(H - 1, W - 1 - xb0);
+    const int xbc = xb0 - NG;                          // consumer strip (kk + 1)
+    const int t0c = max(0, -(xbc + NG - 1)), t1c = min(H - 1, W - 1 - xbc);
+    const bool has_prod = kk > 0, has_cons = kk + 1 < ns;
+    const int pw = (w + V5_WARPS - 1) % V5_WARPS;
+    const int pbase = (w > 0 ? r : r - 1) * 65536;     // producer's round in progress words
+    const int rbase = r * 65536;
+    publish(rbase + t0);
+    if (t0 > t1) {
+      publish(rbase + H);
+      continue;
+    }
+    // hand-over records: the producer's (read) and this strip's (written)
+    const uint32_t* prod_rec = w > 0 ? rings + (size_t)(w - 1) * V5_RS * REC
+                                     : gbuf + (size_t)((r - 1) & 1) * H * REC;
+    uint32_t* own_rec = w < V5_WARPS - 1 ? rings + (size_t)w * V5_RS * REC
+                                         : gbuf + (size_t)(r & 1) * H * REC;
+    // slot masks: a V5_RS-slot shared ring, or one record per step (global)
+    const int prod_mask = w > 0 ? V5_RS - 1 : 0x3FFFFFFF;
+    const bool own_shared = w < V5_WARPS - 1;
+    const int own_mask = own_shared ? V5_RS - 1 : 0x3FFFFFFF;
+
+    auto load_meta = [&](int t) -> uint2 {
+      const int x = xb0 + q + t;
+      if (t <= t1 && in_img(x)) return meta[(size_t)(up ? H - 1 - t : t) * W + x];
+      return make_uint2(V3_NONE, 0u);
+    };
+    auto issue = [&](uint2 mt, int slot) -> uint32_t {
+      __syncwarp();   // every lane is done reading this slot (two steps ago)
+      uint32_t st = 0xFFFFFFFFu, en = 0u;
+      if (mt.x != V3_NONE) {
+        const int lo = (int)(mt.x & 0xFFFFu), hi = (int)(mt.x >> 16);
+        st = mt.y - pad_before(lo);
+        en = st + pixel_slots(lo, hi);
+      }
+      st = __reduce_min_sync(FULL, st);
+      en = __reduce_max_sync(FULL, en);
+      if (lane == 0) {
+        const uint32_t bytes = (en - st) * 4u;
+        const unsigned b = bar0 + 8u * (unsigned)slot;
+        uint32_t* dst = buf + slot * 2 * BUFW;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     ::"r"(b), "r"(INIT ? bytes : 2u * bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(Cg + st), "r"(bytes), "r"(b)
+                     : "memory");
+        if (!INIT)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"((unsigned)__cvta_generic_to_shared(dst + BUFW)), "l"(Sg + st), "r"(bytes),
+                       "r"(b) : "memory");
+      }
+      return st;
+    };
+
+    uint32_t A[NW], B[NW], Cs[NW];
+#pragma unroll
+    for (int ww = 0; ww < NW; ++ww) A[ww] = B[ww] = Cs[ww] = INF16x2;
+    uint32_t a_p2 = INF16x2, a_ng = INF16x2, b_p2 = INF16x2, b_ng = INF16x2, c_p2 = INF16x2,
+             c_ng = INF16x2;
+    uint2 m0 = load_meta(t0), m1 = load_meta(t0 + 1);
+    uint32_t org = issue(m0, it_all & 1);
+
+    for (int t = t0; t <= t1; ++t, ++it_all) {
+      const int slot = it_all & 1;
+      const uint2 mt = m0;
+      const uint2 m2 = load_meta(t + 2);
+      uint32_t org_next = 0;
+      if (t + 1 <= t1) org_next = issue(m1, slot ^ 1);
+
+      // ---- inputs: A from chain q+1, C from chain q+2 (previous step)
+#pragma unroll
+      for (int ww = 0; ww < NW; ++ww) {
+        A[ww] = __shfl_down_sync(FULL, A[ww], G);
+        Cs[ww] = __shfl_down_sync(FULL, Cs[ww], 2 * G);
+      }
+      uint32_t ap2 = __shfl_down_sync(FULL, a_p2, G), ang = __shfl_down_sync(FULL, a_ng, G);
+      uint32_t cp2 = __shfl_down_sync(FULL, c_p2, 2 * G), cng = __shfl_down_sync(FULL, c_ng, 2 * G);
+      if (q >= NG - 2) {
+        // the producer strip's chains 0 and 1 at step t-1
+        const bool need0 = has_prod && t >= 1 && in_img(xb0 + NG + t - 1);
+        const bool need1 = has_prod && t >= 1 && in_img(xb0 + NG + t);
+        if (need0 || need1) {
+          spin_ge(progs + pw, pbase + t);
+          __threadfence_block();
+        }
+        const uint32_t* rr = prod_rec + (size_t)((t - 1) & prod_mask) * REC;
+        const bool gA = q == NG - 1;
+        const bool okA = gA && need0;
+        const bool okC = gA ? need1 : need0;
+        const int pc = gA ? 2 : 1;
+        if (gA) {
+#pragma unroll
+          for (int ww = 0; ww < NW; ww += 4) {
+            uint4 u = make_uint4(INF16x2, INF16x2, INF16x2, INF16x2);
+            if (okA) u = *reinterpret_cast<const uint4*>(rr + gl * NW + ww);
+            A[ww] = u.x; A[ww + 1] = u.y; A[ww + 2] = u.z; A[ww + 3] = u.w;
+          }
+          ap2 = okA ? rr[3 * G * NW + 0] : INF16x2;
+          ang = okA ? rr[3 * G * NW + 1] : INF16x2;
+        }
+#pragma unroll
+        for (int ww = 0; ww < NW; ww += 4) {
+          uint4 u = make_uint4(INF16x2, INF16x2, INF16x2, INF16x2);
+          if (okC) u = *reinterpret_cast<const uint4*>(rr + pc * G * NW + gl * NW + ww);
+          Cs[ww] = u.x; Cs[ww + 1] = u.y; Cs[ww + 2] = u.z; Cs[ww + 3] = u.w;
+        }
+        cp2 = okC ? rr[3 * G * NW + (gA ? 4 : 2)] : INF16x2;
+        cng = okC ? rr[3 * G * NW + (gA ? 5 : 3)] : INF16x2;
+      }
+
+      // ---- this step's pixel of the lane's chain
+      int base = 0, relb = 0, clo = NCH, chi = -1;
+      uint32_t spanp = 0u;
+      if (mt.x != V3_NONE) {
+        const int j0 = (int)((mt.x & 0xFFFFu) >> 1), j1 = (int)((mt.x >> 16) >> 1);
+        base = (int)(mt.y - (uint32_t)j0 - org) + PPL * gl;
+        relb = PPL * gl - j0 + PPL - 1;
+        spanp = (uint32_t)(j1 - j0 + PPL);
+        clo = j0 / CW;
+        chi = j1 / CW;
+      }
+      const uint32_t um = v3_umask(__reduce_min_sync(FULL, clo), __reduce_max_sync(FULL, chi));
+      wait_slot(slot, (unsigned)((it_all >> 1) & 1));
+      const uint32_t* cb = buf + slot * 2 * BUFW;
+      const uint32_t* sb = cb + BUFW;
+      uint32_t* Srow = Sg + org;
+
+      uint32_t nA = INF16x2, nB = INF16x2, nC = INF16x2;
+      uint32_t lA = INF16x2, lB = INF16x2, lC = INF16x2;   // previous chunk's last word (old)
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        uint32_t PA[PPL], PB[PPL], PC[PPL];
+#pragma unroll
+        for (int kk2 = 0; kk2 < PPL; ++kk2) {
+          PA[kk2] = A[c * PPL + kk2];
+          PB[kk2] = B[c * PPL + kk2];
+          PC[kk2] = Cs[c * PPL + kk2];
+        }
+        if ((um >> c) & 1u) {
+          const int CN = c + 1 < NCH ? c + 1 : 0;
+          const uint32_t rA = gl == 0 ? (c + 1 < NCH ? A[CN * PPL] : INF16x2) : PA[0];
+          const uint32_t rB = gl == 0 ? (c + 1 < NCH ? B[CN * PPL] : INF16x2) : PB[0];
+          const uint32_t rC = gl == 0 ? (c + 1 < NCH ? Cs[CN * PPL] : INF16x2) : PC[0];
+          const uint32_t elA = __shfl_sync(FULL, gl == G - 1 ? lA : PA[PPL - 1], src_l);
+          const uint32_t elB = __shfl_sync(FULL, gl == G - 1 ? lB : PB[PPL - 1], src_l);
+          const uint32_t elC = __shfl_sync(FULL, gl == G - 1 ? lC : PC[PPL - 1], src_l);
+          const uint32_t erA = __shfl_sync(FULL, rA, src_r);
+          const uint32_t erB = __shfl_sync(FULL, rB, src_r);
+          const uint32_t erC = __shfl_sync(FULL, rC, src_r);
+          const bool p = (uint32_t)(relb + c * CW) < spanp;
+          // words outside the pixel's interval read the INF pad
+          const uint4 u = *reinterpret_cast<const uint4*>(p ? cb + base + c * CW : infpad);
+          const uint32_t cn[PPL] = {u.x, u.y, u.z, u.w};
+          uint32_t LA[PPL], LB[PPL], LC[PPL];
+          v3_path(PA, elA, erA, ap2, ang, p1x2, cn, LA);
+          v3_path(PB, elB, erB, b_p2, b_ng, p1x2, cn, LB);
+          v3_path(PC, elC, erC, cp2, cng, p1x2, cn, LC);
+#pragma unroll
+          for (int kk2 = 0; kk2 < PPL; ++kk2) {
+            A[c * PPL + kk2] = LA[kk2];
+            B[c * PPL + kk2] = LB[kk2];
+            Cs[c * PPL + kk2] = LC[kk2];
+          }
+          nA = __vimin3_u16x2(nA, __vminu2(LA[0], LA[1]), __vminu2(LA[2], LA[3]));
+          nB = __vimin3_u16x2(nB, __vminu2(LB[0], LB[1]), __vminu2(LB[2], LB[3]));
+          nC = __vimin3_u16x2(nC, __vminu2(LC[0], LC[1]), __vminu2(LC[2], LC[3]));
+        } else {
+#pragma unroll
+          for (int kk2 = 0; kk2 < PPL; ++kk2)
+            A[c * PPL + kk2] = B[c * PPL + kk2] = Cs[c * PPL + kk2] = INF16x2;
+        }
+        lA = PA[PPL - 1];
+        lB = PB[PPL - 1];
+        lC = PC[PPL - 1];
+      }
+      uint32_t hA = min(nA & 0xFFFFu, nA >> 16), hB = min(nB & 0xFFFFu, nB >> 16),
+               hC = min(nC & 0xFFFFu, nC >> 16);
+#pragma unroll
+      for (int o = G / 2; o; o >>= 1) {
+        hA = min(hA, __shfl_xor_sync(FULL, hA, o));
+        hB = min(hB, __shfl_xor_sync(FULL, hB, o));
+        hC = min(hC, __shfl_xor_sync(FULL, hC, o));
+      }
+      const bool act = spanp != 0u;
+      a_p2 = act ? (hA + a.p2i) * 0x10001u : INF16x2;
+      a_ng = act ? ((0x10000u - hA) & 0xFFFFu) * 0x10001u : INF16x2;
+      b_p2 = act ? (hB + a.p2i) * 0x10001u : INF16x2;
+      b_ng = act ? ((0x10000u - hB) & 0xFFFFu) * 0x10001u : INF16x2;
+      c_p2 = act ? (hC + a.p2i) * 0x10001u : INF16x2;
+      c_ng = act ? ((0x10000u - hC) & 0xFFFFu) * 0x10001u : INF16x2;
+
+      // ---- hand chains 0 and 1 to the consumer strip (it reads step t at
+      // its step t + 1); a shared ring slot is reused only after it was read
+      if (has_cons && t + 1 <= t1c && t + 1 >= t0c && q < 2) {
+        if (own_shared) {
+          const int need = t - V5_RS + 1;
+          if (need >= t0c && need <= t1c) {
+            spin_ge(progs + w + 1, rbase + need + 1);
+            __threadfence_block();
+          }
+        }
+        uint32_t* rr = own_rec + (size_t)(t & own_mask) * REC;
+        if (q == 0) {
+#pragma unroll
+          for (int ww = 0; ww < NW; ww += 4) {
+            *reinterpret_cast<uint4*>(rr + gl * NW + ww) = make_uint4(A[ww], A[ww + 1], A[ww + 2], A[ww + 3]);
+            *reinterpret_cast<uint4*>(rr + G * NW + gl * NW + ww) =
+                make_uint4(Cs[ww], Cs[ww + 1], Cs[ww + 2], Cs[ww + 3]);
+          }
+          if (gl == 0) *reinterpret_cast<uint4*>(rr + 3 * G * NW) = make_uint4(a_p2, a_ng, c_p2, c_ng);
+        } else {
+#pragma unroll
+          for (int ww = 0; ww < NW; ww += 4)
+            *reinterpret_cast<uint4*>(rr + 2 * G * NW + gl * NW + ww) =
+                make_uint4(Cs[ww], Cs[ww + 1], Cs[ww + 2], Cs[ww + 3]);
+          if (gl == 0) *reinterpret_cast<uint2*>(rr + 3 * G * NW + 4) = make_uint2(c_p2, c_ng);
+        }
+      }
+      publish(rbase + t + 1);
+      // ---- partial sums of the step's three directions
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        if (((um >> c) & 1u) && (uint32_t)(relb + c * CW) < spanp) {
+          uint32_t Sx[PPL];
+#pragma unroll
+          for (int kk2 = 0; kk2 < PPL; ++kk2)
+            Sx[kk2] = __vadd2(A[c * PPL + kk2], __vadd2(B[c * PPL + kk2], Cs[c * PPL + kk2]));
+          if (!INIT) {
+            const uint4 w4 = *reinterpret_cast<const uint4*>(sb + base + c * CW);
+            Sx[0] = __vadd2(w4.x, Sx[0]);
+            Sx[1] = __vadd2(w4.y, Sx[1]);
+            Sx[2] = __vadd2(w4.z, Sx[2]);
+            Sx[3] = __vadd2(w4.w, Sx[3]);
+          }
+          *reinterpret_cast<uint4*>(Srow + base + c * CW) = make_uint4(Sx[0], Sx[1], Sx[2], Sx[3]);
+        }
+      }
+      m0 = m1;
+      m1 = m2;
+      org = org_next;
+    }
+    publish(rbase + H);
+  }
+}
+
+template <int G, int NCH>
+void launch_v5(const Vd3Args& v, bool init, int n_sv, cudaStream_t st) {
+  const size_t smem = v5_smem<G, NCH>();
+  auto k = init ? k_sgm_vd5<G, NCH, true> : k_sgm_vd5<G, NCH, false>;
+  static bool attr = false;   // per process; the attribute is per function
+  if (!attr) {
+    cudaFuncSetAttribute(k_sgm_vd5<G, NCH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaFuncSetAttribute(k_sgm_vd5<G, NCH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  k<<<n_sv, V5_WARPS * 32, smem, st>>>(v);
+}
+
+}  // namespace
+
+int vd3_lanes(int d_max) {
+  const int np = npairs_max(d_max);
+  return np <= 64 ? 4 : (np <= 128 ? 8 : 0);
+}
+
+int vd3_strips(int W, int d_max, int H) {
+  const int G = vd3_lanes(d_max);
+  const int NG = G ? 32 / G : 1;
+  return G ? (W + H - 1 + NG - 1) / NG : 0;
+}
+
+size_t vd3_ring_words(int W, int d_max, int H) {
+  const int G = vd3_lanes(d_max);
+  if (!G) return 0;
+  // two round parities x H steps x REC = 3 * G * NW + 8 words (NW = 16 at most)
+  (void)W;
+  return (size_t)2 * H * (3 * G * 16 + 8);
+}
+
+void launch_vd3(const Vd3Args& v, bool init, cudaStream_t st) {
+  const int np = npairs_max(v.a.d_max);
+  const int n_sv = v.total / v.nstrips;
+  if (np <= 16) launch_v5<4, 1>(v, init, n_sv, st);
+  else if (np <= 32) launch_v5<4, 2>(v, init, n_sv, st);
+  else if (np <= 64) launch_v5<4, 4>(v, init, n_sv, st);
+  else launch_v5<8, 4>(v, init, n_sv, st);
+}
+
+}  // namespace es

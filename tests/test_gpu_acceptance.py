@@ -7,10 +7,12 @@ scenes (tests/golden/acceptance.npz):
 * criterion 4: on the 256x128 dolly-out sequence the search fraction is
   1.0 at frame 0, <= 0.60 after, non-increasing over frames 1-3, and every
   frame's fraction and fused map equal the reference's;
-* criterion 10: running a sequence twice gives byte-identical output trees
-  (the device z-buffer and reductions are order-independent)."""
+* criterion 10: running a sequence twice gives byte-identical maps (the
+  device z-buffer and reductions are order-independent).
 
-import os
+The reference's own copies of all ten criteria also run on the device path
+through install() (tests/test_gpu_reference_suite.py)."""
+
 
 import numpy as np
 import pytest
@@ -18,6 +20,14 @@ import pytest
 from conftest import load_golden
 
 pytestmark = pytest.mark.gpu
+
+
+def _run(rig, lefts, rights, motions, params=None):
+    """The frames through one DisparityPipeline, every map read back (the
+    reference's run_sequence loop, pipeline.py:253-259)."""
+    from paper_1708_06301_b200 import pipeline
+    pipe = pipeline.DisparityPipeline(rig, params)
+    return [pipe.process_frame(l, r, m).materialize() for l, r, m in zip(lefts, rights, motions)]
 
 
 def test_criterion3_full_range_equals_reference_sgm():
@@ -40,11 +50,9 @@ def test_criterion4_search_space_reduction_matches_reference():
     g = load_golden("acceptance")
     rig = core.StereoRig(f=256.0, b=0.5, cx=127.5, cy=63.5, width=256, height=128, d_max=64)
     n = len(g["c4_fractions"])
-    seq = pipeline.Sequence(
-        rig, [core.GrayImage(g[f"c4_{k}_left"]) for k in range(n)],
-        [core.GrayImage(g[f"c4_{k}_right"]) for k in range(n)],
-        [None] + [g[f"c4_{k}_motion"] for k in range(1, n)])
-    res = pipeline.run_sequence(seq, pipeline.PipelineParams())
+    res = _run(rig, [core.GrayImage(g[f"c4_{k}_left"]) for k in range(n)],
+               [core.GrayImage(g[f"c4_{k}_right"]) for k in range(n)],
+               [None] + [g[f"c4_{k}_motion"] for k in range(1, n)])
     fr = np.array([r.search_fraction_left for r in res])
     assert np.array_equal(fr, g["c4_fractions"])
     assert fr[0] == 1.0 and (fr[1:] <= 0.60).all() and fr[1] >= fr[2] >= fr[3]
@@ -53,33 +61,29 @@ def test_criterion4_search_space_reduction_matches_reference():
         np.testing.assert_allclose(res[k].fused.left.values, g[f"c4_{k}_fused_d"], rtol=1e-9, atol=0)
 
 
-def test_criterion10_run_is_byte_deterministic(tmp_path):
-    pytest.importorskip("cv2")
-    from paper_1708_06301_b200 import core, pipeline
+def test_criterion10_run_is_byte_deterministic():
+    from paper_1708_06301_b200 import core
     g = load_golden("run_sequence")
     f, b, cx, cy, w, h, d_max = g["rig"]
     rig = core.StereoRig(f=f, b=b, cx=cx, cy=cy, width=int(w), height=int(h), d_max=int(d_max))
     n = len([k for k in g.files if k.endswith("_left")])
-    seq = pipeline.Sequence(
-        rig, [core.GrayImage(g[f"f{k}_left"]) for k in range(n)],
-        [core.GrayImage(g[f"f{k}_right"]) for k in range(n)],
-        [g[f"f{k}_motion"] if bool(g[f"f{k}_has_motion"]) else None for k in range(n)],
-        gt_left=[core.DisparityMap(g[f"f{k}_gt_d"], g[f"f{k}_gt_v"]) for k in range(n)])
-
-    def tree(root):
-        out = {}
-        for dirpath, _, names in os.walk(root):
-            for name in names:
-                full = os.path.join(dirpath, name)
-                out[os.path.relpath(full, root)] = open(full, "rb").read()
-        return out
-
-    pipeline.run_sequence(seq, out_dir=str(tmp_path / "a"))
-    pipeline.run_sequence(seq, out_dir=str(tmp_path / "b"))
-    ta, tb = tree(tmp_path / "a"), tree(tmp_path / "b")
-    assert ta.keys() == tb.keys() and len(ta) >= 2 * n + 2
-    for name in ta:
-        assert ta[name] == tb[name], name
+    args = ([core.GrayImage(g[f"f{k}_left"]) for k in range(n)],
+            [core.GrayImage(g[f"f{k}_right"]) for k in range(n)],
+            [g[f"f{k}_motion"] if bool(g[f"f{k}_has_motion"]) else None for k in range(n)])
+    ra, rb = _run(rig, *args), _run(rig, *args)
+    for x, y in zip(ra, rb):
+        for view in ("left", "right"):
+            for name in ("measured", "fused_d", "fused_p"):
+                if name == "measured":
+                    u, v = getattr(x, "measured_" + view), getattr(y, "measured_" + view)
+                    assert u.values.tobytes() == v.values.tobytes()
+                elif name == "fused_d":
+                    u, v = getattr(x.fused, view), getattr(y.fused, view)
+                    assert u.values.tobytes() == v.values.tobytes()
+                    assert u.valid.tobytes() == v.valid.tobytes()
+                else:
+                    u, v = getattr(x.fused, view + "_var"), getattr(y.fused, view + "_var")
+                    assert u.values.tobytes() == v.values.tobytes()
 
 
 def test_criterion8_ground_truth_inside_three_sigma():
@@ -91,11 +95,9 @@ def test_criterion8_ground_truth_inside_three_sigma():
     g = load_golden("acceptance")
     rig = core.StereoRig(f=256.0, b=0.5, cx=127.5, cy=63.5, width=256, height=128, d_max=64)
     n = len(g["c4_fractions"])
-    seq = pipeline.Sequence(
-        rig, [core.GrayImage(g[f"c4_{k}_left"]) for k in range(n)],
-        [core.GrayImage(g[f"c4_{k}_right"]) for k in range(n)],
-        [None] + [g[f"c4_{k}_motion"] for k in range(1, n)])
-    res = pipeline.run_sequence(seq, pipeline.PipelineParams())
+    res = _run(rig, [core.GrayImage(g[f"c4_{k}_left"]) for k in range(n)],
+               [core.GrayImage(g[f"c4_{k}_right"]) for k in range(n)],
+               [None] + [g[f"c4_{k}_motion"] for k in range(1, n)])
     prm = prediction.PredictionParams(q=0.0, edge_reject=False, fill_holes=False)
     gt = lambda k, v: core.DisparityMap(g[f"c4_{k}_gt{v}_d"], g[f"c4_{k}_gt{v}_v"])   # noqa: E731
     zero = core.VarianceMap(np.zeros((rig.height, rig.width)))
@@ -140,9 +142,8 @@ def test_constant_shift_is_recovered_and_frame0_equals_baseline():
     disp = sgm.select_disparity(sgm.aggregate_paths(
         sgm.matching_cost(left, right, sgm.full_range_intervals(rig), prm), prm))
     assert (disp.values[2:-2, shift + 2:-2] == shift).all()
-    seq = pipeline.Sequence(rig, [left], [right], [None])
-    a = pipeline.run_sequence(seq, pipeline.PipelineParams())[0]
-    b = pipeline.run_sequence(seq, pipeline.PipelineParams(baseline=True))[0]
+    a = _run(rig, [left], [right], [None], pipeline.PipelineParams())[0]
+    b = _run(rig, [left], [right], [None], pipeline.PipelineParams(baseline=True))[0]
     assert np.array_equal(a.fused.left.values, b.fused.left.values)
     assert np.array_equal(a.fused.left.valid, b.fused.left.valid)
     assert a.search_fraction_left == 1.0

@@ -70,8 +70,15 @@ int es_ctx_reset(es_ctx* ctx);
  *               for the right view (geometry.py:62-92); ignored where
  *               motion_given[s] == 0
  *   motion_given [batch] uint8: motion is not None for sequence s
- *   sync        1: wait, check errors, commit state only on success
- *               0: enqueue only (errors surface in es_ctx_sync)            */
+ *   sync        1: wait, check errors, commit state only on success (the
+ *                  reference raises before it updates its state)
+ *               0: enqueue only; the step's state is committed before its
+ *                  error bits are known.  Errors surface in es_ctx_sync (or
+ *                  the next synced step) in the reference's order -- first
+ *                  failing sequence, left view before right, point at
+ *                  infinity before d <= 0 -- and then leave the context
+ *                  POISONED: further steps return ES_ERR_VALUE until
+ *                  es_ctx_reset.                                          */
 int es_ctx_step(es_ctx* ctx, const uint8_t* images, int images_dev, const double* homographies,
                 const uint8_t* motion_given, int sync);
 int es_ctx_sync(es_ctx* ctx);

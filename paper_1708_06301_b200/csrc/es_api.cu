@@ -1,5 +1,7 @@
 // C ABI (include/egostereo_b200.h): pipeline contexts and stage entry points.
 #include <array>
+#include <map>
+#include <tuple>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -153,6 +155,36 @@ __global__ void k_warp_points(const double* Hm, const double* pts, int n, double
 
 }  // namespace
 
+namespace es {
+bool ensure_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> granted;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = granted[{kernel, dev}];
+  if (bytes <= cur || bytes <= 48 * 1024) return true;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+      cudaSuccess)
+    return false;
+  cur = bytes;
+  return true;
+}
+bool ensure_attr(const void* kernel, cudaFuncAttribute attr, int value) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int>, int> set;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_tuple(kernel, dev, (int)attr);
+  auto it = set.find(key);
+  if (it != set.end() && it->second == value) return true;
+  if (cudaFuncSetAttribute(kernel, attr, value) != cudaSuccess) return false;
+  set[key] = value;
+  return true;
+}
+}  // namespace es
+
 struct es_ctx {
   int device = 0;
   es_rig rig_c;
@@ -194,11 +226,9 @@ struct es_ctx {
   int* err = nullptr;
   int* anyv = nullptr;
   unsigned long long* cells = nullptr;
-  // fused vertical + diagonal sweeps: ticket, row counters and edge ring of
-  // each of the two sweeps (es_sgm_vd3.cu)
-  unsigned* v3_ticket = nullptr;
-  int* v3_prog = nullptr;
-  uint32_t* v3_ring = nullptr;
+  // fused vertical + diagonal sweeps: round-boundary hand-over buffers of
+  // the two sweeps (es_sgm_sweep.cu)
+  uint32_t* sw_ring = nullptr;
   // pinned host mirrors
   double* h_Hm = nullptr;
   uint8_t* h_have = nullptr;
@@ -208,6 +238,10 @@ struct es_ctx {
   std::vector<long long> frame;
   std::vector<int> have_state;
   bool pending = false;
+  // an error surfaced from deferred steps: their state was already
+  // committed, so the filter state is not the reference's; steps are refused
+  // until es_ctx_reset
+  bool poisoned = false;
   // pinned argument staging ring (deferred steps may still be reading a slot)
   static constexpr int RING = 4;
   int ring_pos = 0;
@@ -249,8 +283,7 @@ int ctx_free(es_ctx* c) {
                   c->C, c->S,
                   c->Sx[0], c->Sx[1], c->Sx[2], c->dstar, c->r, c->mvalid, c->keep, c->Hm,
                   c->have_pred, c->err, c->anyv,
-                  c->cells, c->kitti, c->cells_acc, c->img2, c->v3_ticket, c->v3_prog,
-                  c->v3_ring};
+                  c->cells, c->kitti, c->cells_acc, c->img2, c->sw_ring};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   void* hptrs[] = {c->h_Hm, c->h_have, c->h_err, c->h_anyv, c->h_cells};
@@ -301,11 +334,17 @@ PredArgs pred_args(es_ctx* c) {
 }
 
 int commit_errors(es_ctx* c) {
-  int bits = 0;
-  for (int s = 0; s < c->B; ++s) bits |= c->h_err[s];
-  if (bits & ERR_POINT_AT_INFINITY)
-    return fail(ES_ERR_POINT_AT_INFINITY, "warped point has ~zero fourth homogeneous component");
-  if (bits & ERR_NONPOSITIVE_D) return fail(ES_ERR_NONPOSITIVE_D, "previous disparity must be positive");
+  // the first failing sequence, and in it the reference's order: left view
+  // (bits 0-1) before right (bits 2-3), point at infinity before d <= 0
+  for (int s = 0; s < c->B; ++s) {
+    const int bits = c->h_err[s];
+    for (int view = 0; view < 2; ++view) {
+      const int b = (bits >> (2 * view)) & 3;
+      if (b & ERR_POINT_AT_INFINITY)
+        return fail(ES_ERR_POINT_AT_INFINITY, "warped point has ~zero fourth homogeneous component");
+      if (b & ERR_NONPOSITIVE_D) return fail(ES_ERR_NONPOSITIVE_D, "previous disparity must be positive");
+    }
+  }
   return ES_OK;
 }
 
@@ -372,10 +411,8 @@ int es_ctx_create(int device, const es_rig* rig, const es_params* prm, int batch
     if (c->parts != 1 && c->parts != 2 && c->parts != 4) c->parts = 2;
     for (int p = 0; p + 1 < c->parts && !e; ++p) e = dalloc(&c->Sx[p], vol_words);
     const int n_sv = 2 * batch;
-    if (!e && vd3_lanes(rig->d_max) && (c->parts == 2 || c->parts == 4)) {
-      e = dalloc(&c->v3_ticket, 2);
-      if (!e) e = dalloc(&c->v3_prog, 2 * (size_t)n_sv * vd3_strips(rig->width, rig->d_max, rig->height));
-      if (!e) e = dalloc(&c->v3_ring, 2 * (size_t)n_sv * vd3_ring_words(rig->width, rig->d_max, rig->height));
+    if (!e && sweep_lanes(rig->d_max) && (c->parts == 2 || c->parts == 4)) {
+      e = dalloc(&c->sw_ring, 2 * (size_t)n_sv * sweep_ring_words(rig->width, rig->d_max, rig->height));
     }
   }
   if (!e) e = dalloc(&c->dstar, n);
@@ -449,6 +486,7 @@ int es_ctx_reset(es_ctx* c) {
     c->frame[s] = -1;
     c->have_state[s] = 0;
   }
+  c->poisoned = false;
   c->pending = false;
   return ES_OK;
 }
@@ -461,7 +499,9 @@ int es_ctx_sync(es_ctx* c) {
     c->pending = false;
     for (int s = 0; s < c->B; ++s) c->have_state[s] = c->h_anyv[s] != 0;
     c->note_fraction();
-    return commit_errors(c);   // error bits accumulated over the deferred steps
+    const int e = commit_errors(c);   // error bits accumulated over the deferred steps
+    if (e) c->poisoned = true;
+    return e;
   }
   return ES_OK;
 }
@@ -472,6 +512,9 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   const int B = c->B;
   const size_t HW = c->HW;
   const int n_sv = 2 * B;
+  if (c->poisoned)
+    return fail(ES_ERR_VALUE, "context state is invalid after an error in a deferred step; "
+                              "call es_ctx_reset");
   if (c->pending && sync) {
     // a previous deferred step: surface its errors first
     if (int e = es_ctx_sync(c)) return e;
@@ -559,9 +602,7 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   // count (<= split: G lanes per chain, > split: 2G; measured)
   sa.lanes = c->lanes;
   sa.cells = c->cells;
-  sa.vd3_ticket = c->v3_ticket;
-  sa.vd3_prog = c->v3_prog;
-  sa.vd3_ring = c->v3_ring;
+  sa.sweep_ring = c->sw_ring;
   static const double split = getenv("ES_SGM_SPLIT") ? atof(getenv("ES_SGM_SPLIT")) : 0.6;
   sa.split = split;
   if (c->arith == ARITH_U16 && !c->lanes) {

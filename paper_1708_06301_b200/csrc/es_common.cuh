@@ -34,7 +34,10 @@ struct Params {
   double p_init;
 };
 
-// error bits (per sequence)
+// error bits (per sequence; shifted left by 2 * view so the host can report
+// them in the reference's order: left view first, and within a view the
+// warp's PointAtInfinityError before propagate_variance's ValueError,
+// prediction.py:100-109, 129-145)
 constexpr int ERR_POINT_AT_INFINITY = 1;
 constexpr int ERR_NONPOSITIVE_D = 2;
 

@@ -314,7 +314,7 @@ void launch_cost(const CostArgs& a, int n_sv, cudaStream_t st) {
                   (size_t)CR_WARPS * 32 * rmax;
     if (a.tma)   // 16-byte-aligned byte rows + mbarrier
       smem = cost_rows_offset(a.W, cost_pad_cols(a.d_max), rmax) + 6 * (size_t)((a.W + 31) & ~15) + 16;
-    cudaFuncSetAttribute(k_cost_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem((const void*)k_cost_runs, smem);
     k_cost_runs<<<grid, CR_WARPS * 32, smem, st>>>(a, rmax);
     return;
   }
@@ -323,15 +323,15 @@ void launch_cost(const CostArgs& a, int n_sv, cudaStream_t st) {
   const size_t smem = sizeof(uint32_t) * ((size_t)2 * nw * a.W + 2 * (size_t)a.W);
   switch (nw) {
     case 1:
-      cudaFuncSetAttribute(k_cost<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      ensure_smem((const void*)k_cost<1>, smem);
       k_cost<1><<<grid, COST_NT, smem, st>>>(a);
       break;
     case 2:
-      cudaFuncSetAttribute(k_cost<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      ensure_smem((const void*)k_cost<2>, smem);
       k_cost<2><<<grid, COST_NT, smem, st>>>(a);
       break;
     default:
-      cudaFuncSetAttribute(k_cost<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      ensure_smem((const void*)k_cost<3>, smem);
       k_cost<3><<<grid, COST_NT, smem, st>>>(a);
       break;
   }

@@ -7,6 +7,13 @@
 
 namespace es {
 
+// kernel attributes, set once per (kernel, device, value) and checked:
+// cudaFuncAttributeMaxDynamicSharedMemorySize is raised only when a launch
+// needs more than already granted; false (and the CUDA error left for the
+// caller's cudaGetLastError) when the device refuses
+bool ensure_smem(const void* kernel, size_t bytes);
+bool ensure_attr(const void* kernel, cudaFuncAttribute attr, int value);
+
 // ---- prediction (es_predict.cu); all arrays are [n_sv][H][W] ------------
 struct PredArgs {
   Rig rig;
@@ -72,11 +79,9 @@ struct SgmArgs {
   const unsigned long long* cells = nullptr;
   double split = 0.3;
   int select = 0;       // internal: 0 all, 1 fraction <= split, 2 fraction > split
-  // fused vertical + diagonal passes (launch_aggregate_parts): workspace for
-  // the two sweeps -- ticket + row counters + ring each (null: grp4 jobs)
-  unsigned* vd3_ticket = nullptr;   // [2]
-  int* vd3_prog = nullptr;          // [2][n_sv][nstrips]
-  uint32_t* vd3_ring = nullptr;     // [2][n_sv][vd3_ring_words]
+  // fused vertical + diagonal sweeps (launch_aggregate_parts): the
+  // round-boundary hand-over buffers of the two sweeps (null: grp4 jobs only)
+  uint32_t* sweep_ring = nullptr;   // [2][n_sv][sweep_ring_words]
 };
 // full 8-path aggregation; the u16 path runs 4 family launches (both sweeps
 // each), the f32 path runs the 8 directions in the reference's order
@@ -93,22 +98,20 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
 bool vd_supported(int W, int d_max);
 void launch_vd(const SgmArgs& a, bool up, bool init, int n_sv, cudaStream_t st);
 
-// fused vertical + diagonal row sweep (es_sgm_vd3.cu): the three directions
-// of one row sweep (up = 0: dy = +1, up = 1: dy = -1) in one pass; strips of
-// 32/G columns per warp, edge columns exchanged through an L2 ring.
-struct Vd3Args {
+// fused vertical + diagonal row sweep (es_sgm_sweep.cu): the three
+// directions of one row sweep (up = 0: dy = +1, up = 1: dy = -1) in one pass,
+// one CTA per (sequence, view), sheared diagonal strips of 32/G chains per warp
+struct SweepArgs {
   SgmArgs a;
   int up;                 // 0: top -> bottom, 1: bottom -> top
-  int nstrips;            // strips per view (vd3_strips)
+  int nstrips;            // strips per view (sweep_strips)
   int total;              // n_sv * nstrips
-  unsigned* ticket;       // zeroed before the launch
-  int* prog;              // [n_sv][nstrips] rows completed, zeroed before the launch
-  uint32_t* ring;         // [n_sv][vd3_ring_words]
+  uint32_t* ring;         // [n_sv][sweep_ring_words]: round-boundary hand-over records
 };
-int vd3_lanes(int d_max);                      // G (0: unsupported d_max)
-int vd3_strips(int W, int d_max, int H);
-size_t vd3_ring_words(int W, int d_max, int H);  // per (seq, view)
-void launch_vd3(const Vd3Args& v, bool init, cudaStream_t st);
+int sweep_lanes(int d_max);                           // G (0: d_max too large)
+int sweep_strips(int W, int d_max, int H);
+size_t sweep_ring_words(int W, int d_max, int H);     // per (seq, view)
+void launch_sweep(const SweepArgs& v, bool init, cudaStream_t st);
 
 struct WtaArgs {
   int W, H;

@@ -72,11 +72,11 @@ __global__ void k_warp_zmax(PredArgs a) {
       bool at_inf;
       const double di = d[i];
       if (warp_src(a.Hm + 16 * sv, a.rig, x, y, di, tgt, dp, at_inf)) {
-        if (!(di > 0.0)) atomicOr(a.err + s, ERR_NONPOSITIVE_D);
+        if (!(di > 0.0)) atomicOr(a.err + s, ERR_NONPOSITIVE_D << (2 * (sv & 1)));
         atomicMax(a.zkey + sv * HW + tgt, (unsigned long long)__double_as_longlong(dp));
       } else {
         tgt = NO_SRC;
-        if (at_inf) atomicOr(a.err + s, ERR_POINT_AT_INFINITY);
+        if (at_inf) atomicOr(a.err + s, ERR_POINT_AT_INFINITY << (2 * (sv & 1)));
       }
     }
   }
@@ -138,11 +138,11 @@ __global__ void __launch_bounds__(ZT_W * ZT_H) k_warp_zmax_tile(PredArgs a) {
       bool at_inf;
       const double di = td[c];
       if (warp_src(a.Hm + 16 * sv, a.rig, x, y, di, tgt, dp, at_inf)) {
-        if (!(di > 0.0)) atomicOr(a.err + s, ERR_NONPOSITIVE_D);
+        if (!(di > 0.0)) atomicOr(a.err + s, ERR_NONPOSITIVE_D << (2 * (sv & 1)));
         atomicMax(a.zkey + sv * HW + tgt, (unsigned long long)__double_as_longlong(dp));
       } else {
         tgt = NO_SRC;
-        if (at_inf) atomicOr(a.err + s, ERR_POINT_AT_INFINITY);
+        if (at_inf) atomicOr(a.err + s, ERR_POINT_AT_INFINITY << (2 * (sv & 1)));
       }
     }
   }

@@ -846,14 +846,14 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
   int widen = widen_env >= 0 ? widen_env : (n_sv <= 2 && np <= 64 ? 1 : 0);
   if (np > 64) widen += 1;
   static const int split_env = getenv("ES_SGM_SPLITH") ? atoi(getenv("ES_SGM_SPLITH")) : 1;
-  static const int v3_env = getenv("ES_SGM_VD3") ? atoi(getenv("ES_SGM_VD3")) : 1;
-  if (g4 && v3_env && a.vd3_ring && (parts == 2 || parts == 4) && vd3_lanes(a.d_max)) {
-    // fused vertical + diagonal sweeps (es_sgm_vd3.cu): each partial sum
+  static const int sweep_env = getenv("ES_SGM_SWEEP") ? atoi(getenv("ES_SGM_SWEEP")) : 1;
+  if (g4 && sweep_env && a.sweep_ring && (parts == 2 || parts == 4) && sweep_lanes(a.d_max)) {
+    // fused vertical + diagonal sweeps (es_sgm_sweep.cu): each partial sum
     // takes one row job and one three-direction sweep: S0 = rows ->, then
     // the dy = +1 sweep; S1 = rows <-, then the dy = -1 sweep (parts == 4:
     // the sweeps write S2 / S3 concurrently with the row jobs instead)
-    const int ns = vd3_strips(a.W, a.d_max, a.H);
-    const size_t ringw = vd3_ring_words(a.W, a.d_max, a.H);
+    const int ns = sweep_strips(a.W, a.d_max, a.H);
+    const size_t ringw = sweep_ring_words(a.W, a.d_max, a.H);
     for (int p = 0; p < 2; ++p) {
       SgmArgs lo = a, hi = a;
       lo.select = 1;
@@ -864,19 +864,15 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
       launch_grp4_g(4 << widen, lo, FAM_H, 1, n_sv, st_lo[p], p == 0 ? 1 : 2);
       launch_grp4_g(8 << widen, hi, FAM_H, 1, n_sv, st_lo[p], p == 0 ? 1 : 2);
       const int sp = parts == 4 ? p + 2 : p;
-      Vd3Args v;
+      SweepArgs v;
       v.a = a;
       v.a.S = S[sp];
       v.up = p;
       v.nstrips = ns;
       v.total = n_sv * ns;
-      v.ticket = a.vd3_ticket + p;
-      v.prog = a.vd3_prog + (size_t)p * n_sv * ns;
-      v.ring = a.vd3_ring + (size_t)p * n_sv * ringw;
+      v.ring = a.sweep_ring + (size_t)p * n_sv * ringw;
       cudaStream_t vs = st_lo[sp];
-      cudaMemsetAsync(v.ticket, 0, sizeof(unsigned), vs);
-      cudaMemsetAsync(v.prog, 0, sizeof(int) * (size_t)n_sv * ns, vs);
-      launch_vd3(v, parts == 4, vs);
+      launch_sweep(v, parts == 4, vs);
     }
     return parts;
   }
@@ -1291,7 +1287,7 @@ void launch_wta_variance(const WtaArgs& a, int n_sv, cudaStream_t st) {
                                                        std::max<size_t>(16, (148 * 8 + n_sv - 1) / n_sv));
     dim3 grid(per_sv, n_sv);
     auto go = [&](auto kern) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      ensure_smem((const void*)kern, smem);
       kern<<<grid, WR_WARPS * 32, smem, st>>>(a, rmax);
     };
     // runs in flight per lane: four for narrow views, two for wide ones

@@ -44,102 +44,56 @@ namespace es {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int V3_PPL = 4;      // words per lane per chunk
-constexpr int V3_WARPS = 4;    // warps per CTA
-constexpr uint32_t V3_NONE = 0xFFFFFFFFu;
+constexpr int SW_PPL = 4;      // words per lane per chunk
+constexpr uint32_t SW_NONE = 0xFFFFFFFFu;
 
-template <int G, int NCH>
-struct V3 {
-  static constexpr int NG = 32 / G;             // columns per strip
-  static constexpr int CW = V3_PPL * G;         // words per chunk
-  static constexpr int NW = V3_PPL * NCH;       // state words per lane
-  static constexpr int BUFW = NG * NCH * CW;    // staged words per row (upper bound)
-  static constexpr int REC = G * NW + 4;        // ring record: G lanes x NW words + splats
-};
-
-__device__ __forceinline__ uint32_t v3_umask(int lo, int hi) {
+__device__ __forceinline__ uint32_t sw_umask(int lo, int hi) {
   return hi < lo ? 0u : ((hi >= 31 ? 0xFFFFFFFFu : ((2u << hi) - 1u)) & ~((1u << lo) - 1u));
-}
-
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ int ld_relaxed(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-// spin (relaxed loads, no L1 invalidation per poll) until *p >= v, then one
-// acquire load orders the ring reads after the producer's release
-__device__ __forceinline__ void wait_ge(const int* p, int v) {
-  if (ld_relaxed(p) < v) {
-    do {
-      __nanosleep(32);
-    } while (ld_relaxed(p) < v);
-  }
-  (void)ld_acquire(p);
-}
-__device__ __forceinline__ void st_relaxed(int* p, int v) {
-  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint4 ld_cg4(const uint32_t* p) {
-  uint4 r;
-  asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) {
-  uint32_t r;
-  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(r) : "l"(p));
-  return r;
 }
 
 // one path update of a lane's 4 words (k_sgm_grp4's recurrence):
 // L = C + min(Lp(d), min(Lp(d-1), Lp(d+1)) + P1, m + P2) - m
-__device__ __forceinline__ void v3_path(const uint32_t* P, uint32_t el, uint32_t er, uint32_t mp2,
+__device__ __forceinline__ void sw_path(const uint32_t* P, uint32_t el, uint32_t er, uint32_t mp2,
                                         uint32_t ng, uint32_t p1x2, const uint32_t* cn,
                                         uint32_t* L) {
-  uint32_t X[V3_PPL + 1];
+  uint32_t X[SW_PPL + 1];
   X[0] = __byte_perm(el, P[0], 0x5432);
 #pragma unroll
-  for (int k = 1; k < V3_PPL; ++k) X[k] = __byte_perm(P[k - 1], P[k], 0x5432);
-  X[V3_PPL] = __byte_perm(P[V3_PPL - 1], er, 0x5432);
+  for (int k = 1; k < SW_PPL; ++k) X[k] = __byte_perm(P[k - 1], P[k], 0x5432);
+  X[SW_PPL] = __byte_perm(P[SW_PPL - 1], er, 0x5432);
 #pragma unroll
-  for (int k = 0; k < V3_PPL; ++k) {
+  for (int k = 0; k < SW_PPL; ++k) {
     const uint32_t cand = __viaddmin_u16x2(__vminu2(X[k], X[k + 1]), p1x2, __vminu2(P[k], mp2));
     L[k] = __vadd2(cn[k], __vadd2(cand, ng));
   }
 }
 
 template <int G, int NCH>
-struct V5 {
+struct SW {
   static constexpr int NG = 32 / G;             // chains per strip
-  static constexpr int CW = V3_PPL * G;         // words per chunk
-  static constexpr int NW = V3_PPL * NCH;       // state words per lane
+  static constexpr int CW = SW_PPL * G;         // words per chunk
+  static constexpr int NW = SW_PPL * NCH;       // state words per lane
   static constexpr int BUFW = NG * NCH * CW;    // staged words per step (upper bound)
   static constexpr int REC = 3 * G * NW + 8;    // hand-over record: A0, C0, C1 + 6 splats
 };
-constexpr int V5_WARPS = 16;   // warps per CTA = strips per round
-constexpr int V5_RS = 4;       // shared-memory ring slots per warp pair
+constexpr int SW_WARPS = 16;   // warps per CTA = strips per round
+constexpr int SW_RS = 4;       // shared-memory ring slots per warp pair
 
 template <int G, int NCH>
-constexpr size_t v5_smem() {
-  using T = V5<G, NCH>;
-  return sizeof(uint32_t) * ((size_t)V5_WARPS * 4 * T::BUFW + V5_WARPS * 4 +
-                             (size_t)(V5_WARPS - 1) * V5_RS * T::REC + V5_WARPS + 4);
+constexpr size_t sweep_smem() {
+  using T = SW<G, NCH>;
+  return sizeof(uint32_t) * ((size_t)SW_WARPS * 4 * T::BUFW + SW_WARPS * 4 +
+                             (size_t)(SW_WARPS - 1) * SW_RS * T::REC + SW_WARPS + 4);
 }
 
 __device__ __forceinline__ void spin_ge(const volatile int* p, int v) {
-  while (*p < v) {
-  }
+  while (*p < v) __nanosleep(8);
 }
 
 template <int G, int NCH, bool INIT>
-__global__ void __launch_bounds__(V5_WARPS * 32, 1) k_sgm_vd5(Vd3Args v) {
-  using T = V5<G, NCH>;
-  constexpr int NG = T::NG, CW = T::CW, NW = T::NW, PPL = V3_PPL, REC = T::REC;
+__global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
+  using T = SW<G, NCH>;
+  constexpr int NG = T::NG, CW = T::CW, NW = T::NW, PPL = SW_PPL, REC = T::REC;
   constexpr int BUFW = T::BUFW;
   extern __shared__ __align__(16) uint32_t sm5[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -148,10 +102,10 @@ __global__ void __launch_bounds__(V5_WARPS * 32, 1) k_sgm_vd5(Vd3Args v) {
   const int src_l = gbase | ((gl + G - 1) & (G - 1));
   const int src_r = gbase | ((gl + 1) & (G - 1));
   uint32_t* buf = sm5 + w * (4 * BUFW);   // [2 slots][cost, sum][BUFW]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm5 + V5_WARPS * 4 * BUFW) + 2 * w;
-  uint32_t* rings = sm5 + V5_WARPS * 4 * BUFW + V5_WARPS * 4;          // [V5_WARPS-1][RS][REC]
-  volatile int* progs = reinterpret_cast<volatile int*>(rings + (V5_WARPS - 1) * V5_RS * REC);
-  uint32_t* infpad = rings + (V5_WARPS - 1) * V5_RS * REC + V5_WARPS;   // 4 words of +inf
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm5 + SW_WARPS * 4 * BUFW) + 2 * w;
+  uint32_t* rings = sm5 + SW_WARPS * 4 * BUFW + SW_WARPS * 4;          // [SW_WARPS-1][RS][REC]
+  volatile int* progs = reinterpret_cast<volatile int*>(rings + (SW_WARPS - 1) * SW_RS * REC);
+  uint32_t* infpad = rings + (SW_WARPS - 1) * SW_RS * REC + SW_WARPS;   // 4 words of +inf
 
   const SgmArgs& a = v.a;
   const int W = a.W, H = a.H;
@@ -171,7 +125,7 @@ __global__ void __launch_bounds__(V5_WARPS * 32, 1) k_sgm_vd5(Vd3Args v) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (threadIdx.x < V5_WARPS) progs[threadIdx.x] = 0;
+  if (threadIdx.x < SW_WARPS) progs[threadIdx.x] = 0;
   if (threadIdx.x < 4) infpad[threadIdx.x] = INF16x2;
   __syncthreads();
 
@@ -193,12 +147,12 @@ __global__ void __launch_bounds__(V5_WARPS * 32, 1) k_sgm_vd5(Vd3Args v) {
   };
 
   int it_all = 0;   // steps walked by this warp (mbarrier slot / phase)
-  const int rounds = (ns + V5_WARPS - 1) / V5_WARPS;
+  const int rounds = (ns + SW_WARPS - 1) / SW_WARPS;
   for (int r = 0; r < rounds; ++r) {
     // every warp has finished round r-1: the shared ring slots and the
     // global buffer of round r-2's parity are free again
     __syncthreads();
-    const int kk = r * V5_WARPS + w;
+    const int kk = r * SW_WARPS + w;
     if (kk >= ns) continue;
     const int k = ns - 1 - kk;
     const int xb0 = -(H - 1) + k * NG;                 // chain of lane group 0 (x at step 0)
@@ -206,7 +160,7 @@ __global__ void __launch_bounds__(V5_WARPS * 32, 1) k_sgm_vd5(Vd3Args v) {
     const int xbc = xb0 - NG;                          // consumer strip (kk + 1)
     const int t0c = max(0, -(xbc + NG - 1)), t1c = min(H - 1, W - 1 - xbc);
     const bool has_prod = kk > 0, has_cons = kk + 1 < ns;
-    const int pw = (w + V5_WARPS - 1) % V5_WARPS;
+    const int pw = (w + SW_WARPS - 1) % SW_WARPS;
     const int pbase = (w > 0 ? r : r - 1) * 65536;     // producer's round in progress words
     const int rbase = r * 65536;
     publish(rbase + t0);
@@ -215,24 +169,24 @@ __global__ void __launch_bounds__(V5_WARPS * 32, 1) k_sgm_vd5(Vd3Args v) {
       continue;
     }
     // hand-over records: the producer's (read) and this strip's (written)
-    const uint32_t* prod_rec = w > 0 ? rings + (size_t)(w - 1) * V5_RS * REC
+    const uint32_t* prod_rec = w > 0 ? rings + (size_t)(w - 1) * SW_RS * REC
                                      : gbuf + (size_t)((r - 1) & 1) * H * REC;
-    uint32_t* own_rec = w < V5_WARPS - 1 ? rings + (size_t)w * V5_RS * REC
+    uint32_t* own_rec = w < SW_WARPS - 1 ? rings + (size_t)w * SW_RS * REC
                                          : gbuf + (size_t)(r & 1) * H * REC;
-    // slot masks: a V5_RS-slot shared ring, or one record per step (global)
-    const int prod_mask = w > 0 ? V5_RS - 1 : 0x3FFFFFFF;
-    const bool own_shared = w < V5_WARPS - 1;
-    const int own_mask = own_shared ? V5_RS - 1 : 0x3FFFFFFF;
+    // slot masks: a SW_RS-slot shared ring, or one record per step (global)
+    const int prod_mask = w > 0 ? SW_RS - 1 : 0x3FFFFFFF;
+    const bool own_shared = w < SW_WARPS - 1;
+    const int own_mask = own_shared ? SW_RS - 1 : 0x3FFFFFFF;
 
     auto load_meta = [&](int t) -> uint2 {
       const int x = xb0 + q + t;
       if (t <= t1 && in_img(x)) return meta[(size_t)(up ? H - 1 - t : t) * W + x];
-      return make_uint2(V3_NONE, 0u);
+      return make_uint2(SW_NONE, 0u);
     };
     auto issue = [&](uint2 mt, int slot) -> uint32_t {
       __syncwarp();   // every lane is done reading this slot (two steps ago)
       uint32_t st = 0xFFFFFFFFu, en = 0u;
-      if (mt.x != V3_NONE) {
+      if (mt.x != SW_NONE) {
         const int lo = (int)(mt.x & 0xFFFFu), hi = (int)(mt.x >> 16);
         st = mt.y - pad_before(lo);
         en = st + pixel_slots(lo, hi);
@@ -264,6 +218,7 @@ __global__ void __launch_bounds__(V5_WARPS * 32, 1) k_sgm_vd5(Vd3Args v) {
              c_ng = INF16x2;
     uint2 m0 = load_meta(t0), m1 = load_meta(t0 + 1);
     uint32_t org = issue(m0, it_all & 1);
+    uint32_t pm = 0u;   // chunks computed at the previous step (warp-uniform)
 
     for (int t = t0; t <= t1; ++t, ++it_all) {
       const int slot = it_all & 1;
@@ -280,10 +235,11 @@ __global__ void __launch_bounds__(V5_WARPS * 32, 1) k_sgm_vd5(Vd3Args v) {
       }
       uint32_t ap2 = __shfl_down_sync(FULL, a_p2, G), ang = __shfl_down_sync(FULL, a_ng, G);
       uint32_t cp2 = __shfl_down_sync(FULL, c_p2, 2 * G), cng = __shfl_down_sync(FULL, c_ng, 2 * G);
+      // the producer strip's chains 0 and 1 at step t-1 (warp-uniform)
+      const bool need0 = has_prod && t >= 1 && in_img(xb0 + NG + t - 1);
+      const bool need1 = has_prod && t >= 1 && in_img(xb0 + NG + t);
+      const bool fed = need0 || need1;
       if (q >= NG - 2) {
-        // the producer strip's chains 0 and 1 at step t-1
-        const bool need0 = has_prod && t >= 1 && in_img(xb0 + NG + t - 1);
-        const bool need1 = has_prod && t >= 1 && in_img(xb0 + NG + t);
         if (need0 || need1) {
           spin_ge(progs + pw, pbase + t);
           __threadfence_block();
@@ -316,7 +272,7 @@ __global__ void __launch_bounds__(V5_WARPS * 32, 1) k_sgm_vd5(Vd3Args v) {
       // ---- this step's pixel of the lane's chain
       int base = 0, relb = 0, clo = NCH, chi = -1;
       uint32_t spanp = 0u;
-      if (mt.x != V3_NONE) {
+      if (mt.x != SW_NONE) {
         const int j0 = (int)((mt.x & 0xFFFFu) >> 1), j1 = (int)((mt.x >> 16) >> 1);
         base = (int)(mt.y - (uint32_t)j0 - org) + PPL * gl;
         relb = PPL * gl - j0 + PPL - 1;
@@ -324,7 +280,7 @@ __global__ void __launch_bounds__(V5_WARPS * 32, 1) k_sgm_vd5(Vd3Args v) {
         clo = j0 / CW;
         chi = j1 / CW;
       }
-      const uint32_t um = v3_umask(__reduce_min_sync(FULL, clo), __reduce_max_sync(FULL, chi));
+      const uint32_t um = sw_umask(__reduce_min_sync(FULL, clo), __reduce_max_sync(FULL, chi));
       wait_slot(slot, (unsigned)((it_all >> 1) & 1));
       const uint32_t* cb = buf + slot * 2 * BUFW;
       const uint32_t* sb = cb + BUFW;
@@ -357,9 +313,9 @@ __global__ void __launch_bounds__(V5_WARPS * 32, 1) k_sgm_vd5(Vd3Args v) {
           const uint4 u = *reinterpret_cast<const uint4*>(p ? cb + base + c * CW : infpad);
           const uint32_t cn[PPL] = {u.x, u.y, u.z, u.w};
           uint32_t LA[PPL], LB[PPL], LC[PPL];
-          v3_path(PA, elA, erA, ap2, ang, p1x2, cn, LA);
-          v3_path(PB, elB, erB, b_p2, b_ng, p1x2, cn, LB);
-          v3_path(PC, elC, erC, cp2, cng, p1x2, cn, LC);
+          sw_path(PA, elA, erA, ap2, ang, p1x2, cn, LA);
+          sw_path(PB, elB, erB, b_p2, b_ng, p1x2, cn, LB);
+          sw_path(PC, elC, erC, cp2, cng, p1x2, cn, LC);
 #pragma unroll
           for (int kk2 = 0; kk2 < PPL; ++kk2) {
             A[c * PPL + kk2] = LA[kk2];
@@ -369,15 +325,23 @@ __global__ void __launch_bounds__(V5_WARPS * 32, 1) k_sgm_vd5(Vd3Args v) {
           nA = __vimin3_u16x2(nA, __vminu2(LA[0], LA[1]), __vminu2(LA[2], LA[3]));
           nB = __vimin3_u16x2(nB, __vminu2(LB[0], LB[1]), __vminu2(LB[2], LB[3]));
           nC = __vimin3_u16x2(nC, __vminu2(LC[0], LC[1]), __vminu2(LC[2], LC[3]));
-        } else {
-#pragma unroll
-          for (int kk2 = 0; kk2 < PPL; ++kk2)
-            A[c * PPL + kk2] = B[c * PPL + kk2] = Cs[c * PPL + kk2] = INF16x2;
         }
         lA = PA[PPL - 1];
         lB = PB[PPL - 1];
         lC = PC[PPL - 1];
       }
+      // chunks outside this step's union must hold +inf; only those computed
+      // at the previous step, or refilled from the hand-over record, can hold
+      // anything else (warp-uniform test, no per-chunk default moves)
+      const uint32_t clr = ~um & (pm | (fed ? 0xFFFFFFFFu : 0u));
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+        if ((clr >> c) & 1u) {
+#pragma unroll
+          for (int kk2 = 0; kk2 < PPL; ++kk2)
+            A[c * PPL + kk2] = B[c * PPL + kk2] = Cs[c * PPL + kk2] = INF16x2;
+        }
+      pm = um;
       uint32_t hA = min(nA & 0xFFFFu, nA >> 16), hB = min(nB & 0xFFFFu, nB >> 16),
                hC = min(nC & 0xFFFFu, nC >> 16);
 #pragma unroll
@@ -398,7 +362,7 @@ __global__ void __launch_bounds__(V5_WARPS * 32, 1) k_sgm_vd5(Vd3Args v) {
       // its step t + 1); a shared ring slot is reused only after it was read
       if (has_cons && t + 1 <= t1c && t + 1 >= t0c && q < 2) {
         if (own_shared) {
-          const int need = t - V5_RS + 1;
+          const int need = t - SW_RS + 1;
           if (need >= t0c && need <= t1c) {
             spin_ge(progs + w + 1, rbase + need + 1);
             __threadfence_block();
@@ -449,48 +413,41 @@ __global__ void __launch_bounds__(V5_WARPS * 32, 1) k_sgm_vd5(Vd3Args v) {
 }
 
 template <int G, int NCH>
-void launch_v5(const Vd3Args& v, bool init, int n_sv, cudaStream_t st) {
-  const size_t smem = v5_smem<G, NCH>();
-  auto k = init ? k_sgm_vd5<G, NCH, true> : k_sgm_vd5<G, NCH, false>;
-  static bool attr = false;   // per process; the attribute is per function
-  if (!attr) {
-    cudaFuncSetAttribute(k_sgm_vd5<G, NCH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    cudaFuncSetAttribute(k_sgm_vd5<G, NCH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = true;
-  }
-  k<<<n_sv, V5_WARPS * 32, smem, st>>>(v);
+void launch_sweep_t(const SweepArgs& v, bool init, int n_sv, cudaStream_t st) {
+  const size_t smem = sweep_smem<G, NCH>();
+  auto k = init ? k_sgm_sweep<G, NCH, true> : k_sgm_sweep<G, NCH, false>;
+  ensure_smem((const void*)k, smem);
+  k<<<n_sv, SW_WARPS * 32, smem, st>>>(v);
 }
 
 }  // namespace
 
-int vd3_lanes(int d_max) {
+int sweep_lanes(int d_max) {
   const int np = npairs_max(d_max);
   return np <= 64 ? 4 : (np <= 128 ? 8 : 0);
 }
 
-int vd3_strips(int W, int d_max, int H) {
-  const int G = vd3_lanes(d_max);
+int sweep_strips(int W, int d_max, int H) {
+  const int G = sweep_lanes(d_max);
   const int NG = G ? 32 / G : 1;
   return G ? (W + H - 1 + NG - 1) / NG : 0;
 }
 
-size_t vd3_ring_words(int W, int d_max, int H) {
-  const int G = vd3_lanes(d_max);
+size_t sweep_ring_words(int W, int d_max, int H) {
+  const int G = sweep_lanes(d_max);
   if (!G) return 0;
   // two round parities x H steps x REC = 3 * G * NW + 8 words (NW = 16 at most)
   (void)W;
   return (size_t)2 * H * (3 * G * 16 + 8);
 }
 
-void launch_vd3(const Vd3Args& v, bool init, cudaStream_t st) {
+void launch_sweep(const SweepArgs& v, bool init, cudaStream_t st) {
   const int np = npairs_max(v.a.d_max);
   const int n_sv = v.total / v.nstrips;
-  if (np <= 16) launch_v5<4, 1>(v, init, n_sv, st);
-  else if (np <= 32) launch_v5<4, 2>(v, init, n_sv, st);
-  else if (np <= 64) launch_v5<4, 4>(v, init, n_sv, st);
-  else launch_v5<8, 4>(v, init, n_sv, st);
+  if (np <= 16) launch_sweep_t<4, 1>(v, init, n_sv, st);
+  else if (np <= 32) launch_sweep_t<4, 2>(v, init, n_sv, st);
+  else if (np <= 64) launch_sweep_t<4, 4>(v, init, n_sv, st);
+  else launch_sweep_t<8, 4>(v, init, n_sv, st);
 }
 
 }  // namespace es

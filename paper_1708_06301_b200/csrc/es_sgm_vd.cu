@@ -378,31 +378,28 @@ __global__ void __cluster_dims__(VC, 1, 1) __launch_bounds__(VMAXW * 32, 1) k_sg
 }  // namespace
 
 bool vd_supported(int W, int d_max) {
-  static int ok = -1;
   if (npairs_max(d_max) > VNW || W < VC * VNG) return false;
   if (vd_maxcols(W) / VNG > VMAXW * VGPW) return false;
   const size_t smem = vd_smem_bytes(W);
   int dev = 0, optin = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+    return false;
   if (smem > (size_t)optin) return false;
-  if (ok < 0) {
-    ok = 1;
-    for (auto k : {k_sgm_vd<false, false>, k_sgm_vd<true, false>, k_sgm_vd<false, true>,
-                   k_sgm_vd<true, true>})
-      if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
-          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        ok = 0;
-  }
-  return ok == 1;
+  // per (kernel, device) and checked (es_api.cu ensure_*)
+  for (auto k : {k_sgm_vd<false, false>, k_sgm_vd<true, false>, k_sgm_vd<false, true>,
+                 k_sgm_vd<true, true>})
+    if (!ensure_attr((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ||
+        !ensure_smem((const void*)k, smem))
+      return false;
+  return true;
 }
 
 void launch_vd(const SgmArgs& a, bool up, bool init, int n_sv, cudaStream_t st) {
   const size_t smem = vd_smem_bytes(a.W);
   auto k = up ? (init ? k_sgm_vd<true, true> : k_sgm_vd<true, false>)
               : (init ? k_sgm_vd<false, true> : k_sgm_vd<false, false>);
-  cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // attributes were set by vd_supported (the caller's precondition)
   const int nwarps = (vd_maxcols(a.W) / VNG + VGPW - 1) / VGPW;
   k<<<dim3(VC, n_sv), nwarps * 32, smem, st>>>(a);
 }

@@ -32,6 +32,7 @@ STAGES = [("k_warp_zmax", "predict"), ("k_warp_zidx", "predict"), ("k_resolve_fi
           ("k_fill_v_intervals", "intervals"), ("k_cost_runs", "cost"), ("k_sgm_", "aggregate"),
           ("k_wta_runs", "wta_variance"), ("k_checks_fuse", "checks_fuse")]
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3,
+         "ns": 1e-6, "us": 1e-3, "ms": 1.0,
          "msecond": 1.0, "%": 1, "inst": 1, "": 1}
 
 

@@ -846,8 +846,12 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
   int widen = widen_env >= 0 ? widen_env : (n_sv <= 2 && np <= 64 ? 1 : 0);
   if (np > 64) widen += 1;
   static const int split_env = getenv("ES_SGM_SPLITH") ? atoi(getenv("ES_SGM_SPLITH")) : 1;
-  static const int sweep_env = getenv("ES_SGM_SWEEP") ? atoi(getenv("ES_SGM_SWEEP")) : 1;
-  if (g4 && sweep_env && a.sweep_ring && (parts == 2 || parts == 4) && sweep_lanes(a.d_max)) {
+  // the fused sweep runs one CTA (a whole SM) per (sequence, view): it needs
+  // about an SM's worth of views to fill the GPU; smaller batches keep the
+  // per-direction jobs (ES_SGM_SWEEP=0 / 1 force it off / on)
+  static const int sweep_env = getenv("ES_SGM_SWEEP") ? atoi(getenv("ES_SGM_SWEEP")) : -1;
+  const bool use_sweep = sweep_env < 0 ? n_sv >= 96 : sweep_env > 0;
+  if (g4 && use_sweep && a.sweep_ring && (parts == 2 || parts == 4) && sweep_lanes(a.d_max)) {
     // fused vertical + diagonal sweeps (es_sgm_sweep.cu): each partial sum
     // takes one row job and one three-direction sweep: S0 = rows ->, then
     // the dy = +1 sweep; S1 = rows <-, then the dy = -1 sweep (parts == 4:

@@ -11,10 +11,9 @@ the UNMODIFIED reference produced (oracle/make_golden_configs.py):
 
 The device renderer draws the same scenes; the image hashes prove the bytes
 equal synth.render_frame's.  Every map of every frame must then hash-match
-the reference (intervals, WTA disparities, validity / keep masks, matching
-variance, predicted and fused float64 state), and at the digested frames the
-dense cost and aggregated volumes too.  Should a float map ever differ in a
-last bit, its row sums must still agree within the north star's 1e-4."""
+the reference bit for bit (intervals, WTA disparities, validity / keep
+masks, matching variance, predicted and fused float64 state), and at the
+digested frames the dense cost and aggregated volumes too."""
 
 import hashlib
 import glob
@@ -84,9 +83,15 @@ def _check_frame(g, k, res, vols=True):
             if _digest(a) == want:
                 exact += name in FLOAT_MAPS
                 continue
-            assert name in FLOAT_MAPS, (k, v, name, "integer map differs from the reference")
-            np.testing.assert_allclose(a.sum(axis=1), g[f"f{k}_{v}_{name}_rowsum"], rtol=1e-4,
-                                       err_msg=f"frame {k} view {v} map {name}")
+            # bit-exact is the bar (integers and the float64 state); for a float
+            # map report how far the row sums are off (the north star's
+            # tolerance is 1e-4 relative)
+            detail = ""
+            if name in FLOAT_MAPS:
+                ref = g[f"f{k}_{v}_{name}_rowsum"]
+                rel = np.max(np.abs(a.sum(axis=1) - ref) / np.maximum(np.abs(ref), 1e-300))
+                detail = f"max row-sum relative difference {rel:.3e}"
+            raise AssertionError(f"frame {k} view {v} map {name} differs from the reference {detail}")
         c = g[f"f{k}_{v}_counts"]
         assert [int(maps["pred_v"].sum()), int(maps["meas_v"].sum()), int(maps["keep"].sum()),
                 int(maps["fused_v"].sum())] == list(c), (k, v)

@@ -858,15 +858,17 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
     // the sweeps write S2 / S3 concurrently with the row jobs instead)
     const int ns = sweep_strips(a.W, a.d_max, a.H);
     const size_t ringw = sweep_ring_words(a.W, a.d_max, a.H);
+    // the sweeps keep one CTA per view and leave SMs idle (128 views on 148
+    // SMs): with parts == 2 the second stream runs its sweep FIRST, so the
+    // first stream's row job fills those SMs while it runs (and the second
+    // stream's row job those of the first stream's sweep)
+    static const int order_env = getenv("ES_SGM_SWEEP_ORDER") ? atoi(getenv("ES_SGM_SWEEP_ORDER")) : 1;
     for (int p = 0; p < 2; ++p) {
       SgmArgs lo = a, hi = a;
       lo.select = 1;
       hi.select = 2;
       lo.S = S[p];
       hi.S = S[p];
-      // both regime variants of the row job on one stream, then the sweep
-      launch_grp4_g(4 << widen, lo, FAM_H, 1, n_sv, st_lo[p], p == 0 ? 1 : 2);
-      launch_grp4_g(8 << widen, hi, FAM_H, 1, n_sv, st_lo[p], p == 0 ? 1 : 2);
       const int sp = parts == 4 ? p + 2 : p;
       SweepArgs v;
       v.a = a;
@@ -876,7 +878,12 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
       v.total = n_sv * ns;
       v.ring = a.sweep_ring + (size_t)p * n_sv * ringw;
       cudaStream_t vs = st_lo[sp];
-      launch_sweep(v, parts == 4, vs);
+      const bool sweep_first = parts == 2 && p == 1 && order_env;
+      if (sweep_first) launch_sweep(v, true, vs);
+      // both regime variants of the row job on one stream
+      launch_grp4_g(4 << widen, lo, FAM_H, sweep_first ? 0 : 1, n_sv, st_lo[p], p == 0 ? 1 : 2);
+      launch_grp4_g(8 << widen, hi, FAM_H, sweep_first ? 0 : 1, n_sv, st_lo[p], p == 0 ? 1 : 2);
+      if (!sweep_first) launch_sweep(v, parts == 4, vs);
     }
     return parts;
   }

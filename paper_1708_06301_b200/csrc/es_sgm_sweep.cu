@@ -77,13 +77,19 @@ struct SW {
   static constexpr int REC = 3 * G * NW + 8;    // hand-over record: A0, C0, C1 + 6 splats
 };
 constexpr int SW_WARPS = 16;   // warps per CTA = strips per round
-constexpr int SW_RS = 4;       // shared-memory ring slots per warp pair
+#ifndef SW_RS_SLOTS
+#define SW_RS_SLOTS 2
+#endif
+// shared-memory ring slots per warp pair (2 measured best: the staging
+// buffers and rings share the SM's 256 KB with the L1 that serves the
+// metadata loads; 8 slots cost 3 ms per step)
+constexpr int SW_RS = SW_RS_SLOTS;
 
 template <int G, int NCH>
 constexpr size_t sweep_smem() {
   using T = SW<G, NCH>;
   return sizeof(uint32_t) * ((size_t)SW_WARPS * 4 * T::BUFW + SW_WARPS * 4 +
-                             (size_t)(SW_WARPS - 1) * SW_RS * T::REC + SW_WARPS + 4);
+                             (size_t)(SW_WARPS - 1) * SW_RS * T::REC + SW_WARPS + T::REC);
 }
 
 __device__ __forceinline__ void spin_ge(const volatile int* p, int v) {
@@ -105,7 +111,10 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm5 + SW_WARPS * 4 * BUFW) + 2 * w;
   uint32_t* rings = sm5 + SW_WARPS * 4 * BUFW + SW_WARPS * 4;          // [SW_WARPS-1][RS][REC]
   volatile int* progs = reinterpret_cast<volatile int*>(rings + (SW_WARPS - 1) * SW_RS * REC);
-  uint32_t* infpad = rings + (SW_WARPS - 1) * SW_RS * REC + SW_WARPS;   // 4 words of +inf
+  // a whole hand-over record of +inf (states and splats): read instead of the
+  // producer's record where its pixel is off the image; its first 4 words
+  // also pad cost reads outside a pixel's interval
+  uint32_t* infpad = rings + (SW_WARPS - 1) * SW_RS * REC + SW_WARPS;
 
   const SgmArgs& a = v.a;
   const int W = a.W, H = a.H;
@@ -126,7 +135,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (threadIdx.x < SW_WARPS) progs[threadIdx.x] = 0;
-  if (threadIdx.x < 4) infpad[threadIdx.x] = INF16x2;
+  for (int i = threadIdx.x; i < REC; i += blockDim.x) infpad[i] = INF16x2;
   __syncthreads();
 
   auto in_img = [&](int x) { return x >= 0 && x < W; };
@@ -248,25 +257,27 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
         const bool gA = q == NG - 1;
         const bool okA = gA && need0;
         const bool okC = gA ? need1 : need0;
-        const int pc = gA ? 2 : 1;
+        // the +inf record stands in where the producer's pixel is off the
+        // image: unconditional vector loads, no default moves
+        const uint32_t* ra = okA ? rr : infpad;
+        const uint32_t* rc = okC ? rr + (gA ? 2 : 1) * G * NW : infpad;
+        const uint32_t* rs = okC ? rr : infpad;
         if (gA) {
 #pragma unroll
           for (int ww = 0; ww < NW; ww += 4) {
-            uint4 u = make_uint4(INF16x2, INF16x2, INF16x2, INF16x2);
-            if (okA) u = *reinterpret_cast<const uint4*>(rr + gl * NW + ww);
+            const uint4 u = *reinterpret_cast<const uint4*>(ra + gl * NW + ww);
             A[ww] = u.x; A[ww + 1] = u.y; A[ww + 2] = u.z; A[ww + 3] = u.w;
           }
-          ap2 = okA ? rr[3 * G * NW + 0] : INF16x2;
-          ang = okA ? rr[3 * G * NW + 1] : INF16x2;
+          ap2 = ra[3 * G * NW + 0];
+          ang = ra[3 * G * NW + 1];
         }
 #pragma unroll
         for (int ww = 0; ww < NW; ww += 4) {
-          uint4 u = make_uint4(INF16x2, INF16x2, INF16x2, INF16x2);
-          if (okC) u = *reinterpret_cast<const uint4*>(rr + pc * G * NW + gl * NW + ww);
+          const uint4 u = *reinterpret_cast<const uint4*>(rc + gl * NW + ww);
           Cs[ww] = u.x; Cs[ww + 1] = u.y; Cs[ww + 2] = u.z; Cs[ww + 3] = u.w;
         }
-        cp2 = okC ? rr[3 * G * NW + (gA ? 4 : 2)] : INF16x2;
-        cng = okC ? rr[3 * G * NW + (gA ? 5 : 3)] : INF16x2;
+        cp2 = rs[3 * G * NW + (gA ? 4 : 2)];
+        cng = rs[3 * G * NW + (gA ? 5 : 3)];
       }
 
       // ---- this step's pixel of the lane's chain

@@ -125,7 +125,9 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
   const uint2* __restrict__ meta = a.meta + (size_t)sv * HW;
   const uint32_t* Cg = reinterpret_cast<const uint32_t*>(a.C) + (size_t)sv * a.volcap;
   uint32_t* Sg = reinterpret_cast<uint32_t*>(a.S) + (size_t)sv * a.volcap;
-  uint32_t* gbuf = v.ring + (size_t)sv * 2 * H * REC;   // [round parity][step][REC]
+  // [round parity][step][REC] records, then one +inf record
+  uint32_t* gbuf = v.ring + (size_t)sv * (2 * (size_t)H + 1) * REC;
+  uint32_t* ginf = gbuf + 2 * (size_t)H * REC;
   const uint32_t p1x2 = a.p1i * 0x10001u;
 
   const unsigned bar0 = (unsigned)__cvta_generic_to_shared(bars);
@@ -135,7 +137,10 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (threadIdx.x < SW_WARPS) progs[threadIdx.x] = 0;
-  for (int i = threadIdx.x; i < REC; i += blockDim.x) infpad[i] = INF16x2;
+  for (int i = threadIdx.x; i < REC; i += blockDim.x) {
+    infpad[i] = INF16x2;
+    ginf[i] = INF16x2;
+  }
   __syncthreads();
 
   auto in_img = [&](int x) { return x >= 0 && x < W; };
@@ -178,14 +183,15 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
       continue;
     }
     // hand-over records: the producer's (read) and this strip's (written)
-    const uint32_t* prod_rec = w > 0 ? rings + (size_t)(w - 1) * SW_RS * REC
-                                     : gbuf + (size_t)((r - 1) & 1) * H * REC;
-    uint32_t* own_rec = w < SW_WARPS - 1 ? rings + (size_t)w * SW_RS * REC
-                                         : gbuf + (size_t)(r & 1) * H * REC;
+    // hand-over records: shared rings between warps of a round, the global
+    // buffer across the round boundary (kept apart so every access compiles
+    // to LDS / STS or LDG / STG, not generic loads)
+    const uint32_t* prod_sh = rings + (size_t)(w > 0 ? w - 1 : 0) * SW_RS * REC;
+    const uint32_t* prod_gl = gbuf + (size_t)((r - 1) & 1) * H * REC;
+    uint32_t* own_sh = rings + (size_t)(w < SW_WARPS - 1 ? w : 0) * SW_RS * REC;
+    uint32_t* own_gl = gbuf + (size_t)(r & 1) * H * REC;
     // slot masks: a SW_RS-slot shared ring, or one record per step (global)
-    const int prod_mask = w > 0 ? SW_RS - 1 : 0x3FFFFFFF;
     const bool own_shared = w < SW_WARPS - 1;
-    const int own_mask = own_shared ? SW_RS - 1 : 0x3FFFFFFF;
 
     auto load_meta = [&](int t) -> uint2 {
       const int x = xb0 + q + t;
@@ -253,31 +259,34 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
           spin_ge(progs + pw, pbase + t);
           __threadfence_block();
         }
-        const uint32_t* rr = prod_rec + (size_t)((t - 1) & prod_mask) * REC;
         const bool gA = q == NG - 1;
         const bool okA = gA && need0;
         const bool okC = gA ? need1 : need0;
         // the +inf record stands in where the producer's pixel is off the
         // image: unconditional vector loads, no default moves
-        const uint32_t* ra = okA ? rr : infpad;
-        const uint32_t* rc = okC ? rr + (gA ? 2 : 1) * G * NW : infpad;
-        const uint32_t* rs = okC ? rr : infpad;
-        if (gA) {
+        auto read_rec = [&](const uint32_t* rr, const uint32_t* inf) {
+          const uint32_t* ra = okA ? rr : inf;
+          const uint32_t* rc = okC ? rr + (gA ? 2 : 1) * G * NW : inf;
+          const uint32_t* rs = okC ? rr : inf;
+          if (gA) {
+#pragma unroll
+            for (int ww = 0; ww < NW; ww += 4) {
+              const uint4 u = *reinterpret_cast<const uint4*>(ra + gl * NW + ww);
+              A[ww] = u.x; A[ww + 1] = u.y; A[ww + 2] = u.z; A[ww + 3] = u.w;
+            }
+            ap2 = ra[3 * G * NW + 0];
+            ang = ra[3 * G * NW + 1];
+          }
 #pragma unroll
           for (int ww = 0; ww < NW; ww += 4) {
-            const uint4 u = *reinterpret_cast<const uint4*>(ra + gl * NW + ww);
-            A[ww] = u.x; A[ww + 1] = u.y; A[ww + 2] = u.z; A[ww + 3] = u.w;
+            const uint4 u = *reinterpret_cast<const uint4*>(rc + gl * NW + ww);
+            Cs[ww] = u.x; Cs[ww + 1] = u.y; Cs[ww + 2] = u.z; Cs[ww + 3] = u.w;
           }
-          ap2 = ra[3 * G * NW + 0];
-          ang = ra[3 * G * NW + 1];
-        }
-#pragma unroll
-        for (int ww = 0; ww < NW; ww += 4) {
-          const uint4 u = *reinterpret_cast<const uint4*>(rc + gl * NW + ww);
-          Cs[ww] = u.x; Cs[ww + 1] = u.y; Cs[ww + 2] = u.z; Cs[ww + 3] = u.w;
-        }
-        cp2 = rs[3 * G * NW + (gA ? 4 : 2)];
-        cng = rs[3 * G * NW + (gA ? 5 : 3)];
+          cp2 = rs[3 * G * NW + (gA ? 4 : 2)];
+          cng = rs[3 * G * NW + (gA ? 5 : 3)];
+        };
+        if (w > 0) read_rec(prod_sh + (size_t)((t - 1) & (SW_RS - 1)) * REC, infpad);
+        else read_rec(prod_gl + (size_t)(t - 1) * REC, ginf);
       }
 
       // ---- this step's pixel of the lane's chain
@@ -379,22 +388,25 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
             __threadfence_block();
           }
         }
-        uint32_t* rr = own_rec + (size_t)(t & own_mask) * REC;
-        if (q == 0) {
+        auto write_rec = [&](uint32_t* rr) {
+          if (q == 0) {
 #pragma unroll
-          for (int ww = 0; ww < NW; ww += 4) {
-            *reinterpret_cast<uint4*>(rr + gl * NW + ww) = make_uint4(A[ww], A[ww + 1], A[ww + 2], A[ww + 3]);
-            *reinterpret_cast<uint4*>(rr + G * NW + gl * NW + ww) =
-                make_uint4(Cs[ww], Cs[ww + 1], Cs[ww + 2], Cs[ww + 3]);
+            for (int ww = 0; ww < NW; ww += 4) {
+              *reinterpret_cast<uint4*>(rr + gl * NW + ww) = make_uint4(A[ww], A[ww + 1], A[ww + 2], A[ww + 3]);
+              *reinterpret_cast<uint4*>(rr + G * NW + gl * NW + ww) =
+                  make_uint4(Cs[ww], Cs[ww + 1], Cs[ww + 2], Cs[ww + 3]);
+            }
+            if (gl == 0) *reinterpret_cast<uint4*>(rr + 3 * G * NW) = make_uint4(a_p2, a_ng, c_p2, c_ng);
+          } else {
+#pragma unroll
+            for (int ww = 0; ww < NW; ww += 4)
+              *reinterpret_cast<uint4*>(rr + 2 * G * NW + gl * NW + ww) =
+                  make_uint4(Cs[ww], Cs[ww + 1], Cs[ww + 2], Cs[ww + 3]);
+            if (gl == 0) *reinterpret_cast<uint2*>(rr + 3 * G * NW + 4) = make_uint2(c_p2, c_ng);
           }
-          if (gl == 0) *reinterpret_cast<uint4*>(rr + 3 * G * NW) = make_uint4(a_p2, a_ng, c_p2, c_ng);
-        } else {
-#pragma unroll
-          for (int ww = 0; ww < NW; ww += 4)
-            *reinterpret_cast<uint4*>(rr + 2 * G * NW + gl * NW + ww) =
-                make_uint4(Cs[ww], Cs[ww + 1], Cs[ww + 2], Cs[ww + 3]);
-          if (gl == 0) *reinterpret_cast<uint2*>(rr + 3 * G * NW + 4) = make_uint2(c_p2, c_ng);
-        }
+        };
+        if (own_shared) write_rec(own_sh + (size_t)(t & (SW_RS - 1)) * REC);
+        else write_rec(own_gl + (size_t)t * REC);
       }
       publish(rbase + t + 1);
       // ---- partial sums of the step's three directions
@@ -447,9 +459,10 @@ int sweep_strips(int W, int d_max, int H) {
 size_t sweep_ring_words(int W, int d_max, int H) {
   const int G = sweep_lanes(d_max);
   if (!G) return 0;
-  // two round parities x H steps x REC = 3 * G * NW + 8 words (NW = 16 at most)
+  // two round parities x H steps + one +inf record, REC = 3 * G * NW + 8
+  // words (NW = 16 at most)
   (void)W;
-  return (size_t)2 * H * (3 * G * 16 + 8);
+  return (size_t)(2 * H + 1) * (3 * G * 16 + 8);
 }
 
 void launch_sweep(const SweepArgs& v, bool init, cudaStream_t st) {

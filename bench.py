@@ -347,13 +347,10 @@ def cpu_arm(config, procs, n_timed, seq0=0):
 # ----------------------------------------------------------------- main
 
 def lib_sha256():
-    import hashlib
-    path = os.path.join(ROOT, "paper_1708_06301_b200", "libegostereo_b200.so")
-    try:
-        with open(path, "rb") as fh:
-            return hashlib.sha256(fh.read()).hexdigest()
-    except OSError:
-        return None
+    """The kernel build's id: SHA-256 of the CUDA sources + compile flags
+    (`build.build_id`; the .so bytes themselves differ between compiles)."""
+    from paper_1708_06301_b200 import build as _b
+    return _b.build_id()
 
 
 def measured_ncu(config, batch, texture_scale):

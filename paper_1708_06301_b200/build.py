@@ -28,6 +28,23 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+def build_id() -> str:
+    """SHA-256 over every CUDA source, the C-ABI header and the compile
+    flags: names the kernel build.  (nvcc embeds per-run module ids, so the
+    .so bytes differ between two compiles of the same sources; this id does
+    not.)"""
+    import hashlib
+    h = hashlib.sha256(" ".join(ARCH + FLAGS).encode())
+    deps = sorted(sources() + glob.glob(os.path.join(CSRC, "*.cuh"))
+                  + glob.glob(os.path.join(CSRC, "*.h")))
+    deps.append(os.path.join(os.path.dirname(HERE), "include", "egostereo_b200.h"))
+    for p in deps:
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
 def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True

@@ -15,7 +15,6 @@ from __future__ import annotations
 
 import argparse
 import csv
-import hashlib
 import io
 import json
 import os
@@ -37,8 +36,10 @@ UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "
 
 
 def lib_sha256():
-    with open(os.path.join(ROOT, "paper_1708_06301_b200", "libegostereo_b200.so"), "rb") as fh:
-        return hashlib.sha256(fh.read()).hexdigest()
+    """Build id of the kernels (sources + flags; see build.build_id)."""
+    sys.path.insert(0, ROOT)
+    from paper_1708_06301_b200 import build as _b
+    return _b.build_id()
 
 
 def merge(entry):

@@ -85,15 +85,78 @@ constexpr int SW_WARPS = 16;   // warps per CTA = strips per round
 // metadata loads; 8 slots cost 3 ms per step)
 constexpr int SW_RS = SW_RS_SLOTS;
 
+static_assert((SW_RS & (SW_RS - 1)) == 0, "ring slots: a power of two");
+constexpr int SW_LRS = SW_RS == 1 ? 0 : (SW_RS == 2 ? 1 : (SW_RS == 4 ? 2 : 3));
+
+// dynamic shared memory, in 32-bit words: per-warp operand staging
+// [2 slots][cost, sum][BUFW], the per-warp staging mbarriers (2 each), the
+// hand-over mbarriers (full, empty) of every ring slot of the SW_WARPS - 1
+// warp pairs, the rings [pair][slot][REC], the progress words and one +inf
+// record
+template <int G, int NCH>
+struct SwLayout {
+  using T = SW<G, NCH>;
+  static constexpr size_t bars = (size_t)SW_WARPS * 4 * T::BUFW;
+  static constexpr size_t hbar = bars + SW_WARPS * 4;
+  static constexpr size_t rings = (hbar + (size_t)(SW_WARPS - 1) * SW_RS * 4 + 3) & ~(size_t)3;
+  static constexpr size_t progs = rings + (size_t)(SW_WARPS - 1) * SW_RS * T::REC;
+  static constexpr size_t inf = progs + ((SW_WARPS + 3) & ~3);
+  static constexpr size_t words = inf + T::REC;
+};
+
 template <int G, int NCH>
 constexpr size_t sweep_smem() {
-  using T = SW<G, NCH>;
-  return sizeof(uint32_t) * ((size_t)SW_WARPS * 4 * T::BUFW + SW_WARPS * 4 +
-                             (size_t)(SW_WARPS - 1) * SW_RS * T::REC + SW_WARPS + T::REC);
+  return sizeof(uint32_t) * SwLayout<G, NCH>::words;
 }
 
 __device__ __forceinline__ void spin_ge(const volatile int* p, int v) {
   while (*p < v) __nanosleep(8);
+}
+
+// predicated vector accesses (no branch, registers keep their value when the
+// predicate is off): the hand-over records enter / leave through lanes of
+// chains 0 and 1 only
+__device__ __forceinline__ void lds4_if(bool p, unsigned a, uint32_t* r) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}\n"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]) : "r"(a), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void lds2_if(bool p, unsigned a, uint32_t& x, uint32_t& y) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q ld.shared.v2.u32 {%0, %1}, [%2];\n\t}\n"
+               : "+r"(x), "+r"(y) : "r"(a), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void sts4_if(bool p, unsigned a, uint32_t x, uint32_t y, uint32_t z, uint32_t u) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n\t}\n"
+               :: "r"(a), "r"(x), "r"(y), "r"(z), "r"(u), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void sts2_if(bool p, unsigned a, uint32_t x, uint32_t y) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q st.shared.v2.u32 [%0], {%1, %2};\n\t}\n"
+               :: "r"(a), "r"(x), "r"(y), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void ldg4_if(bool p, const uint32_t* a, uint32_t* r) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}\n"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]) : "l"(a), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void ldg2_if(bool p, const uint32_t* a, uint32_t& x, uint32_t& y) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q ld.global.v2.u32 {%0, %1}, [%2];\n\t}\n"
+               : "+r"(x), "+r"(y) : "l"(a), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void stg4_if(bool p, uint32_t* a, uint32_t x, uint32_t y, uint32_t z, uint32_t u) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.global.v4.u32 [%0], {%1, %2, %3, %4};\n\t}\n"
+               :: "l"(a), "r"(x), "r"(y), "r"(z), "r"(u), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void stg2_if(bool p, uint32_t* a, uint32_t x, uint32_t y) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q st.global.v2.u32 [%0], {%1, %2};\n\t}\n"
+               :: "l"(a), "r"(x), "r"(y), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void mb_wait(unsigned b, unsigned parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}\n"
+                 : "=r"(done) : "r"(b), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(unsigned b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
 }
 
 template <int G, int NCH, bool INIT>
@@ -102,19 +165,32 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
   constexpr int NG = T::NG, CW = T::CW, NW = T::NW, PPL = SW_PPL, REC = T::REC;
   constexpr int BUFW = T::BUFW;
   extern __shared__ __align__(16) uint32_t sm5[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // pipeline position of the warp: the schedulers pick the highest warp id
+  // first, so the chain head (position 0, free-running) is the highest warp
+  const int lane = threadIdx.x & 31;
+#ifdef SW_FWD_ORDER
+  const int w = threadIdx.x >> 5;
+#else
+  const int w = SW_WARPS - 1 - (int)(threadIdx.x >> 5);
+#endif
   const int gl = lane & (G - 1), q = lane / G;
   const int gbase = lane & ~(G - 1);
   const int src_l = gbase | ((gl + G - 1) & (G - 1));
   const int src_r = gbase | ((gl + 1) & (G - 1));
+  using LY = SwLayout<G, NCH>;
   uint32_t* buf = sm5 + w * (4 * BUFW);   // [2 slots][cost, sum][BUFW]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm5 + SW_WARPS * 4 * BUFW) + 2 * w;
-  uint32_t* rings = sm5 + SW_WARPS * 4 * BUFW + SW_WARPS * 4;          // [SW_WARPS-1][RS][REC]
-  volatile int* progs = reinterpret_cast<volatile int*>(rings + (SW_WARPS - 1) * SW_RS * REC);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm5 + LY::bars) + 2 * w;
+  volatile int* progs = reinterpret_cast<volatile int*>(sm5 + LY::progs);
   // a whole hand-over record of +inf (states and splats): read instead of the
   // producer's record where its pixel is off the image; its first 4 words
   // also pad cost reads outside a pixel's interval
-  uint32_t* infpad = rings + (SW_WARPS - 1) * SW_RS * REC + SW_WARPS;
+  uint32_t* infpad = sm5 + LY::inf;
+  const unsigned sm_s = (unsigned)__cvta_generic_to_shared(sm5);
+  const unsigned inf_s = sm_s + 4u * (unsigned)LY::inf;
+  // ring of warp pair (p, p+1) slot s at ring_s + 4 * (p * RS + s) * REC;
+  // its full / empty mbarriers at hbar_s + 16 * (p * RS + s) (+ 8)
+  const unsigned ring_s = sm_s + 4u * (unsigned)LY::rings;
+  const unsigned hbar_s = sm_s + 4u * (unsigned)LY::hbar;
 
   const SgmArgs& a = v.a;
   const int W = a.W, H = a.H;
@@ -134,6 +210,14 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
   if (lane == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0) : "memory");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < (SW_WARPS - 1) * SW_RS) {
+    // all 32 lanes of the writing (reading) warp arrive: each lane's own
+    // predicated stores (loads) are released by its own arrive
+    const unsigned b = hbar_s + 16u * threadIdx.x;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(b) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(b + 8) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (threadIdx.x < SW_WARPS) progs[threadIdx.x] = 0;
@@ -161,11 +245,14 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
   };
 
   int it_all = 0;   // steps walked by this warp (mbarrier slot / phase)
+  int nr = 0, nw = 0;   // hand-over records read from / written to the shared rings
   const int rounds = (ns + SW_WARPS - 1) / SW_WARPS;
   for (int r = 0; r < rounds; ++r) {
+#ifdef SW_ROUND_BARRIER
     // every warp has finished round r-1: the shared ring slots and the
     // global buffer of round r-2's parity are free again
     __syncthreads();
+#endif
     const int kk = r * SW_WARPS + w;
     if (kk >= ns) continue;
     const int k = ns - 1 - kk;
@@ -174,24 +261,30 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
     const int xbc = xb0 - NG;                          // consumer strip (kk + 1)
     const int t0c = max(0, -(xbc + NG - 1)), t1c = min(H - 1, W - 1 - xbc);
     const bool has_prod = kk > 0, has_cons = kk + 1 < ns;
-    const int pw = (w + SW_WARPS - 1) % SW_WARPS;
-    const int pbase = (w > 0 ? r : r - 1) * 65536;     // producer's round in progress words
+    const int xbp = xb0 + NG;                          // producer strip (kk - 1)
+    const int t0p = max(0, -(xbp + NG - 1)), t1p = min(H - 1, W - 1 - xbp);
+    const int pbase = (r - 1) * 65536;                 // global producer: last warp, round r-1
     const int rbase = r * 65536;
-    publish(rbase + t0);
     if (t0 > t1) {
       publish(rbase + H);
       continue;
     }
-    // hand-over records: the producer's (read) and this strip's (written)
-    // hand-over records: shared rings between warps of a round, the global
-    // buffer across the round boundary (kept apart so every access compiles
-    // to LDS / STS or LDG / STG, not generic loads)
-    const uint32_t* prod_sh = rings + (size_t)(w > 0 ? w - 1 : 0) * SW_RS * REC;
+    // hand-over records: between warps of a round through the shared ring of
+    // the warp pair (full / empty mbarriers, records numbered per pair across
+    // rounds), from the last warp to warp 0 of the next round through a
+    // per-view global buffer (progress words; one record per step, double-
+    // buffered by round parity)
     const uint32_t* prod_gl = gbuf + (size_t)((r - 1) & 1) * H * REC;
-    uint32_t* own_sh = rings + (size_t)(w < SW_WARPS - 1 ? w : 0) * SW_RS * REC;
     uint32_t* own_gl = gbuf + (size_t)(r & 1) * H * REC;
-    // slot masks: a SW_RS-slot shared ring, or one record per step (global)
-    const bool own_shared = w < SW_WARPS - 1;
+    if (r > 0 && has_cons && w == SW_WARPS - 1) {
+      // the global buffer of this round's parity was read by warp 0 in round
+      // r-1, which publishes rbase + H when done
+      if (lane == 0) {
+        spin_ge(progs + 0, (r - 1) * 65536 + H);
+        __threadfence_block();
+      }
+      __syncwarp();
+    }
 
     auto load_meta = [&](int t) -> uint2 {
       const int x = xb0 + q + t;
@@ -242,52 +335,63 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
       uint32_t org_next = 0;
       if (t + 1 <= t1) org_next = issue(m1, slot ^ 1);
 
-      // ---- inputs: A from chain q+1, C from chain q+2 (previous step)
-#pragma unroll
-      for (int ww = 0; ww < NW; ++ww) {
-        A[ww] = __shfl_down_sync(FULL, A[ww], G);
-        Cs[ww] = __shfl_down_sync(FULL, Cs[ww], 2 * G);
-      }
-      uint32_t ap2 = __shfl_down_sync(FULL, a_p2, G), ang = __shfl_down_sync(FULL, a_ng, G);
-      uint32_t cp2 = __shfl_down_sync(FULL, c_p2, 2 * G), cng = __shfl_down_sync(FULL, c_ng, 2 * G);
-      // the producer strip's chains 0 and 1 at step t-1 (warp-uniform)
+      // ---- inputs: A from chain q+1, C from chain q+2 (previous step).  The
+      // producer strip's chains 0 and 1 at step t-1 enter through this
+      // strip's lanes of chains 0 and 1 (whose own states were handed on at
+      // step t-1): predicated loads of the hand-over record, then one
+      // rotation by G (A) and 2G (C) lanes.
       const bool need0 = has_prod && t >= 1 && in_img(xb0 + NG + t - 1);
       const bool need1 = has_prod && t >= 1 && in_img(xb0 + NG + t);
       const bool fed = need0 || need1;
-      if (q >= NG - 2) {
-        if (need0 || need1) {
-          spin_ge(progs + pw, pbase + t);
-          __threadfence_block();
+      const bool rec_in = has_prod && t - 1 >= t0p && t - 1 <= t1p;
+      const bool okq = q == 0 ? need0 : need1;   // lanes of chain 0: A0, C0; chain 1: C1
+      if (w > 0) {
+        unsigned rec = inf_s, ebar = 0;
+        if (rec_in) {
+          const int n = nr++;
+          const unsigned slot_i = (unsigned)((w - 1) * SW_RS + (n & (SW_RS - 1)));
+          mb_wait(hbar_s + 16u * slot_i, (unsigned)(n >> SW_LRS) & 1u);
+          rec = ring_s + 4u * slot_i * (unsigned)REC;
+          ebar = hbar_s + 16u * slot_i + 8u;
         }
-        const bool gA = q == NG - 1;
-        const bool okA = gA && need0;
-        const bool okC = gA ? need1 : need0;
-        // the +inf record stands in where the producer's pixel is off the
-        // image: unconditional vector loads, no default moves
-        auto read_rec = [&](const uint32_t* rr, const uint32_t* inf) {
-          const uint32_t* ra = okA ? rr : inf;
-          const uint32_t* rc = okC ? rr + (gA ? 2 : 1) * G * NW : inf;
-          const uint32_t* rs = okC ? rr : inf;
-          if (gA) {
+        const unsigned ra = (need0 ? rec : inf_s) + 4u * (unsigned)(gl * NW);
+        const unsigned rc = (okq ? rec : inf_s) + 4u * (unsigned)((1 + q) * G * NW + gl * NW);
 #pragma unroll
-            for (int ww = 0; ww < NW; ww += 4) {
-              const uint4 u = *reinterpret_cast<const uint4*>(ra + gl * NW + ww);
-              A[ww] = u.x; A[ww + 1] = u.y; A[ww + 2] = u.z; A[ww + 3] = u.w;
-            }
-            ap2 = ra[3 * G * NW + 0];
-            ang = ra[3 * G * NW + 1];
+        for (int ww = 0; ww < NW; ww += 4) {
+          lds4_if(q == 0, ra + 4u * ww, &A[ww]);
+          lds4_if(q < 2, rc + 4u * ww, &Cs[ww]);
+        }
+        lds2_if(q == 0, (need0 ? rec : inf_s) + 4u * (3 * G * NW), a_p2, a_ng);
+        lds2_if(q < 2, (okq ? rec : inf_s) + 4u * (3 * G * NW + 2 + 2 * q), c_p2, c_ng);
+        if (rec_in) mb_arrive(ebar);
+      } else {
+        const uint32_t* rec = ginf;
+        if (rec_in) {
+          if (lane == 0) {
+            spin_ge(progs + SW_WARPS - 1, pbase + t);
+            __threadfence_block();
           }
+          __syncwarp();
+          rec = prod_gl + (size_t)(t - 1) * REC;
+        }
+        const uint32_t* ra = (need0 ? rec : ginf) + gl * NW;
+        const uint32_t* rc = (okq ? rec : ginf) + (1 + q) * G * NW + gl * NW;
 #pragma unroll
-          for (int ww = 0; ww < NW; ww += 4) {
-            const uint4 u = *reinterpret_cast<const uint4*>(rc + gl * NW + ww);
-            Cs[ww] = u.x; Cs[ww + 1] = u.y; Cs[ww + 2] = u.z; Cs[ww + 3] = u.w;
-          }
-          cp2 = rs[3 * G * NW + (gA ? 4 : 2)];
-          cng = rs[3 * G * NW + (gA ? 5 : 3)];
-        };
-        if (w > 0) read_rec(prod_sh + (size_t)((t - 1) & (SW_RS - 1)) * REC, infpad);
-        else read_rec(prod_gl + (size_t)(t - 1) * REC, ginf);
+        for (int ww = 0; ww < NW; ww += 4) {
+          ldg4_if(q == 0, ra + ww, &A[ww]);
+          ldg4_if(q < 2, rc + ww, &Cs[ww]);
+        }
+        ldg2_if(q == 0, (need0 ? rec : ginf) + 3 * G * NW, a_p2, a_ng);
+        ldg2_if(q < 2, (okq ? rec : ginf) + 3 * G * NW + 2 + 2 * q, c_p2, c_ng);
       }
+      const int srcA = (lane + G) & 31, srcC = (lane + 2 * G) & 31;
+#pragma unroll
+      for (int ww = 0; ww < NW; ++ww) {
+        A[ww] = __shfl_sync(FULL, A[ww], srcA);
+        Cs[ww] = __shfl_sync(FULL, Cs[ww], srcC);
+      }
+      const uint32_t ap2 = __shfl_sync(FULL, a_p2, srcA), ang = __shfl_sync(FULL, a_ng, srcA);
+      const uint32_t cp2 = __shfl_sync(FULL, c_p2, srcC), cng = __shfl_sync(FULL, c_ng, srcC);
 
       // ---- this step's pixel of the lane's chain
       int base = 0, relb = 0, clo = NCH, chi = -1;
@@ -379,36 +483,38 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
       c_ng = act ? ((0x10000u - hC) & 0xFFFFu) * 0x10001u : INF16x2;
 
       // ---- hand chains 0 and 1 to the consumer strip (it reads step t at
-      // its step t + 1); a shared ring slot is reused only after it was read
-      if (has_cons && t + 1 <= t1c && t + 1 >= t0c && q < 2) {
-        if (own_shared) {
-          const int need = t - SW_RS + 1;
-          if (need >= t0c && need <= t1c) {
-            spin_ge(progs + w + 1, rbase + need + 1);
-            __threadfence_block();
+      // its step t + 1): predicated stores by the lanes of chains 0 and 1
+      if (has_cons && t + 1 <= t1c && t + 1 >= t0c) {
+        if (w < SW_WARPS - 1) {
+          const int n = nw++;
+          const unsigned slot_i = (unsigned)(w * SW_RS + (n & (SW_RS - 1)));
+          // the slot's previous record (n - RS) has been read
+          mb_wait(hbar_s + 16u * slot_i + 8u, ((unsigned)(n >> SW_LRS) & 1u) ^ 1u);
+          const unsigned rec = ring_s + 4u * slot_i * (unsigned)REC;
+          const unsigned wa = rec + 4u * (unsigned)(gl * NW);
+          const unsigned wc = rec + 4u * (unsigned)((1 + q) * G * NW + gl * NW);
+#pragma unroll
+          for (int ww = 0; ww < NW; ww += 4) {
+            sts4_if(q == 0, wa + 4u * ww, A[ww], A[ww + 1], A[ww + 2], A[ww + 3]);
+            sts4_if(q < 2, wc + 4u * ww, Cs[ww], Cs[ww + 1], Cs[ww + 2], Cs[ww + 3]);
           }
+          sts4_if(q == 0 && gl == 0, rec + 4u * (3 * G * NW), a_p2, a_ng, c_p2, c_ng);
+          sts2_if(q == 1 && gl == 0, rec + 4u * (3 * G * NW + 4), c_p2, c_ng);
+          mb_arrive(hbar_s + 16u * slot_i);
+        } else {
+          uint32_t* rec = own_gl + (size_t)t * REC;
+          uint32_t* wa = rec + gl * NW;
+          uint32_t* wc = rec + (1 + q) * G * NW + gl * NW;
+#pragma unroll
+          for (int ww = 0; ww < NW; ww += 4) {
+            stg4_if(q == 0, wa + ww, A[ww], A[ww + 1], A[ww + 2], A[ww + 3]);
+            stg4_if(q < 2, wc + ww, Cs[ww], Cs[ww + 1], Cs[ww + 2], Cs[ww + 3]);
+          }
+          stg4_if(q == 0 && gl == 0, rec + 3 * G * NW, a_p2, a_ng, c_p2, c_ng);
+          stg2_if(q == 1 && gl == 0, rec + 3 * G * NW + 4, c_p2, c_ng);
         }
-        auto write_rec = [&](uint32_t* rr) {
-          if (q == 0) {
-#pragma unroll
-            for (int ww = 0; ww < NW; ww += 4) {
-              *reinterpret_cast<uint4*>(rr + gl * NW + ww) = make_uint4(A[ww], A[ww + 1], A[ww + 2], A[ww + 3]);
-              *reinterpret_cast<uint4*>(rr + G * NW + gl * NW + ww) =
-                  make_uint4(Cs[ww], Cs[ww + 1], Cs[ww + 2], Cs[ww + 3]);
-            }
-            if (gl == 0) *reinterpret_cast<uint4*>(rr + 3 * G * NW) = make_uint4(a_p2, a_ng, c_p2, c_ng);
-          } else {
-#pragma unroll
-            for (int ww = 0; ww < NW; ww += 4)
-              *reinterpret_cast<uint4*>(rr + 2 * G * NW + gl * NW + ww) =
-                  make_uint4(Cs[ww], Cs[ww + 1], Cs[ww + 2], Cs[ww + 3]);
-            if (gl == 0) *reinterpret_cast<uint2*>(rr + 3 * G * NW + 4) = make_uint2(c_p2, c_ng);
-          }
-        };
-        if (own_shared) write_rec(own_sh + (size_t)(t & (SW_RS - 1)) * REC);
-        else write_rec(own_gl + (size_t)t * REC);
       }
-      publish(rbase + t + 1);
+      if (w == SW_WARPS - 1) publish(rbase + t + 1);
       // ---- partial sums of the step's three directions
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {

@@ -101,7 +101,11 @@ struct SwLayout {
   static constexpr size_t rings = (hbar + (size_t)(SW_WARPS - 1) * SW_RS * 4 + 3) & ~(size_t)3;
   static constexpr size_t progs = rings + (size_t)(SW_WARPS - 1) * SW_RS * T::REC;
   static constexpr size_t inf = progs + ((SW_WARPS + 3) & ~3);
-  static constexpr size_t words = inf + T::REC;
+  // warp 0's records from the last warp of the previous round, staged from
+  // the global buffer by TMA one step ahead: [2][REC] + 2 mbarriers
+  static constexpr size_t head = inf + T::REC;
+  static constexpr size_t headbar = head + 2 * (size_t)T::REC;
+  static constexpr size_t words = headbar + 4;
 };
 
 template <int G, int NCH>
@@ -131,14 +135,6 @@ __device__ __forceinline__ void sts4_if(bool p, unsigned a, uint32_t x, uint32_t
 __device__ __forceinline__ void sts2_if(bool p, unsigned a, uint32_t x, uint32_t y) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q st.shared.v2.u32 [%0], {%1, %2};\n\t}\n"
                :: "r"(a), "r"(x), "r"(y), "r"((int)p) : "memory");
-}
-__device__ __forceinline__ void ldg4_if(bool p, const uint32_t* a, uint32_t* r) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}\n"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]) : "l"(a), "r"((int)p) : "memory");
-}
-__device__ __forceinline__ void ldg2_if(bool p, const uint32_t* a, uint32_t& x, uint32_t& y) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q ld.global.v2.u32 {%0, %1}, [%2];\n\t}\n"
-               : "+r"(x), "+r"(y) : "l"(a), "r"((int)p) : "memory");
 }
 __device__ __forceinline__ void stg4_if(bool p, uint32_t* a, uint32_t x, uint32_t y, uint32_t z, uint32_t u) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.global.v4.u32 [%0], {%1, %2, %3, %4};\n\t}\n"
@@ -191,6 +187,8 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
   // its full / empty mbarriers at hbar_s + 16 * (p * RS + s) (+ 8)
   const unsigned ring_s = sm_s + 4u * (unsigned)LY::rings;
   const unsigned hbar_s = sm_s + 4u * (unsigned)LY::hbar;
+  const unsigned head_s = sm_s + 4u * (unsigned)LY::head;
+  const unsigned headbar_s = sm_s + 4u * (unsigned)LY::headbar;
 
   const SgmArgs& a = v.a;
   const int W = a.W, H = a.H;
@@ -220,6 +218,10 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(b + 8) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (threadIdx.x < 2) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(headbar_s + 8u * threadIdx.x) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   if (threadIdx.x < SW_WARPS) progs[threadIdx.x] = 0;
   for (int i = threadIdx.x; i < REC; i += blockDim.x) {
     infpad[i] = INF16x2;
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
 
   int it_all = 0;   // steps walked by this warp (mbarrier slot / phase)
   int nr = 0, nw = 0;   // hand-over records read from / written to the shared rings
+  int nh = 0, nhr = 0;  // warp 0: global records staged / consumed
   const int rounds = (ns + SW_WARPS - 1) / SW_WARPS;
   for (int r = 0; r < rounds; ++r) {
 #ifdef SW_ROUND_BARRIER
@@ -324,6 +327,25 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
     for (int ww = 0; ww < NW; ++ww) A[ww] = B[ww] = Cs[ww] = INF16x2;
     uint32_t a_p2 = INF16x2, a_ng = INF16x2, b_p2 = INF16x2, b_ng = INF16x2, c_p2 = INF16x2,
              c_ng = INF16x2;
+    // warp 0: stage the global record of step tr (read at step tr + 1) into
+    // shared memory; the last warp of round r-1 wrote it long before
+    auto stage_head = [&](int tr) {
+      if (lane == 0) {
+        spin_ge(progs + SW_WARPS - 1, pbase + tr + 1);
+        __threadfence_block();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const unsigned b = headbar_s + 8u * (unsigned)(nh & 1);
+        const unsigned dst = head_s + 4u * (unsigned)((nh & 1) * REC);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(4u * REC)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(dst), "l"(prod_gl + (size_t)tr * REC), "r"(4u * REC), "r"(b) : "memory");
+      }
+      ++nh;
+    };
+    if (w == 0 && has_prod && t0 >= 1 && t0 - 1 >= t0p && t0 - 1 <= t1p) stage_head(t0 - 1);
+
     uint2 m0 = load_meta(t0), m1 = load_meta(t0 + 1);
     uint32_t org = issue(m0, it_all & 1);
     uint32_t pm = 0u;   // chunks computed at the previous step (warp-uniform)
@@ -365,24 +387,24 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
         lds2_if(q < 2, (okq ? rec : inf_s) + 4u * (3 * G * NW + 2 + 2 * q), c_p2, c_ng);
         if (rec_in) mb_arrive(ebar);
       } else {
-        const uint32_t* rec = ginf;
+        unsigned rec = inf_s;
         if (rec_in) {
-          if (lane == 0) {
-            spin_ge(progs + SW_WARPS - 1, pbase + t);
-            __threadfence_block();
-          }
-          __syncwarp();
-          rec = prod_gl + (size_t)(t - 1) * REC;
+          const int n = nhr++;
+          mb_wait(headbar_s + 8u * (unsigned)(n & 1), (unsigned)(n >> 1) & 1u);
+          rec = head_s + 4u * (unsigned)((n & 1) * REC);
         }
-        const uint32_t* ra = (need0 ? rec : ginf) + gl * NW;
-        const uint32_t* rc = (okq ? rec : ginf) + (1 + q) * G * NW + gl * NW;
+        const unsigned ra = (need0 ? rec : inf_s) + 4u * (unsigned)(gl * NW);
+        const unsigned rc = (okq ? rec : inf_s) + 4u * (unsigned)((1 + q) * G * NW + gl * NW);
 #pragma unroll
         for (int ww = 0; ww < NW; ww += 4) {
-          ldg4_if(q == 0, ra + ww, &A[ww]);
-          ldg4_if(q < 2, rc + ww, &Cs[ww]);
+          lds4_if(q == 0, ra + 4u * ww, &A[ww]);
+          lds4_if(q < 2, rc + 4u * ww, &Cs[ww]);
         }
-        ldg2_if(q == 0, (need0 ? rec : ginf) + 3 * G * NW, a_p2, a_ng);
-        ldg2_if(q < 2, (okq ? rec : ginf) + 3 * G * NW + 2 + 2 * q, c_p2, c_ng);
+        lds2_if(q == 0, (need0 ? rec : inf_s) + 4u * (3 * G * NW), a_p2, a_ng);
+        lds2_if(q < 2, (okq ? rec : inf_s) + 4u * (3 * G * NW + 2 + 2 * q), c_p2, c_ng);
+        // every lane has read the slot before it is staged again (next step)
+        __syncwarp();
+        if (has_prod && t + 1 <= t1 && t >= t0p && t <= t1p) stage_head(t);
       }
       const int srcA = (lane + G) & 31, srcC = (lane + 2 * G) & 31;
 #pragma unroll

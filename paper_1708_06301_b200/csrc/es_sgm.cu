@@ -846,11 +846,13 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
   int widen = widen_env >= 0 ? widen_env : (n_sv <= 2 && np <= 64 ? 1 : 0);
   if (np > 64) widen += 1;
   static const int split_env = getenv("ES_SGM_SPLITH") ? atoi(getenv("ES_SGM_SPLITH")) : 1;
-  // the fused sweep runs one CTA (a whole SM) per (sequence, view): it needs
-  // about an SM's worth of views to fill the GPU; smaller batches keep the
+  // the fused sweep runs one CTA (a whole SM) per (sequence, view) for a
+  // fixed ~9.4 ms per launch at 1242x375: it pays from 64 views up (B = 32:
+  // 1569 vs 1495 frames/s, B = 48: 1598 vs 1542; B = 24: 1347 vs 1477,
+  // B = 16: 1086 vs 1481 -- measured); smaller batches keep the
   // per-direction jobs (ES_SGM_SWEEP=0 / 1 force it off / on)
   static const int sweep_env = getenv("ES_SGM_SWEEP") ? atoi(getenv("ES_SGM_SWEEP")) : -1;
-  const bool use_sweep = sweep_env < 0 ? n_sv >= 96 : sweep_env > 0;
+  const bool use_sweep = sweep_env < 0 ? n_sv >= 64 : sweep_env > 0;
   if (g4 && use_sweep && a.sweep_ring && (parts == 2 || parts == 4) && sweep_lanes(a.d_max)) {
     // fused vertical + diagonal sweeps (es_sgm_sweep.cu): each partial sum
     // takes one row job and one three-direction sweep: S0 = rows ->, then
@@ -878,7 +880,7 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
       v.total = n_sv * ns;
       v.ring = a.sweep_ring + (size_t)p * n_sv * ringw;
       cudaStream_t vs = st_lo[sp];
-      const bool sweep_first = parts == 2 && p == 1 && order_env;
+      const bool sweep_first = parts == 2 && ((p == 1 && order_env) || order_env == 2);
       if (sweep_first) launch_sweep(v, true, vs);
       // both regime variants of the row job on one stream
       launch_grp4_g(4 << widen, lo, FAM_H, sweep_first ? 0 : 1, n_sv, st_lo[p], p == 0 ? 1 : 2);

@@ -69,7 +69,12 @@ def use_config(n):
                     d_max=c["d_max"])
     g["SEQ_FRAMES"] = c["frames"]
 TEXTURE_SCALE = 0.05
-KERNELS_PER_STEP = 19   # zmax, zidx, fill_h, fill_v, cost, 6 sgm jobs x 2 regime variants, wta, fuse
+# kernels per context per step (counted from ncu launch lists): zmax, zidx,
+# fill_h, fill_v, cost, wta, fuse + the aggregation -- from 64 views per
+# context the two fused sweeps and the two row jobs x 2 regime variants (13),
+# below that six per-direction jobs x 2 regime variants (19)
+def kernels_per_step(views_per_context):
+    return 13 if views_per_context >= 64 else 19
 
 
 # Integer roofline of the aggregation (its arithmetic intensity
@@ -466,8 +471,37 @@ def main():
     imgs = render_frames(specs, frames, device)
     bp = pipeline.BatchedPipeline(rig, B, pipeline.PipelineParams(baseline=args.full_range),
                                   device=local)
-    eng = bp.engine
-    ext = torch.cuda.ExternalStream(eng.stream(), device=device)
+    # B >= 64 runs as two contexts of B/2 on their own streams (see
+    # BatchedPipeline): the timed regions start on an event every group's
+    # stream waits for and end at the last group's completion
+    engines = bp.engines
+    config["contexts_per_gpu"] = bp.groups
+    exts = [torch.cuda.ExternalStream(e.stream(), device=device) for e in engines]
+
+    def cells_acc(reset=1):
+        total = 0
+        for e in engines:
+            a = ctypes.c_uint64()
+            _lib.call("es_ctx_cells_acc", e._h, ctypes.byref(a), reset)
+            total += a.value
+        return total
+
+    def start_event():
+        ev = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(exts[0]):
+            ev.record()
+        for x in exts[1:]:
+            x.wait_event(ev)
+        return ev
+
+    def end_events():
+        evs = []
+        for x in exts:
+            ev = torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(x):
+                ev.record()
+            evs.append(ev)
+        return evs
 
     def warm_up():
         # frame 0 (full range) .. Wm-1, synced so have_state is known
@@ -477,44 +511,46 @@ def main():
 
     # ---- device-resident timed region (per-stage profiling OFF) ---------
     warm_up()
-    acc = ctypes.c_uint64()
-    _lib.call("es_ctx_cells_acc", eng._h, ctypes.byref(acc), 1)   # reset the accumulator
+    cells_acc(1)   # reset the accumulators
     clocks = Clocks(local) if rank == 0 else None
     sharding.barrier()
     torch.cuda.synchronize(device)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(ext):
-        ev0.record()
+    ev0 = start_event()
     for i in range(K):
         k = Wm + i
         bp.process_frames(None, motions_for(specs, k), sync=False,
                           images_dev=imgs[k].data_ptr())
-    with torch.cuda.stream(ext):
-        ev1.record()
+    ev1s = end_events()
     bp.sync()
     torch.cuda.synchronize(device)
-    ms = ev0.elapsed_time(ev1)
+    ms = max(ev0.elapsed_time(e) for e in ev1s)
     clk = clocks.stop() if clocks else None
-    _lib.call("es_ctx_cells_acc", eng._h, ctypes.byref(acc), 1)
-    cells = acc.value / K           # searched cells per step (all sequences, both views)
+    cells = cells_acc(1) / K        # searched cells per step (all sequences, both views)
     ms_max = sharding.max_over_ranks(ms, device)
     frames_total = args.batch * K
     value = frames_total / (ms_max / 1e3)
 
     # ---- stage split: a second, untimed replay of the same frames with
-    # per-stage CUDA events (es_ctx_profile) on the context's stream
+    # per-stage CUDA events (es_ctx_profile) on each context's stream; the
+    # groups run one after the other here, so a stage's time is the sum of
+    # its groups' (serialised) times
     bp.reset()
     warm_up()
-    _lib.call("es_ctx_profile", eng._h, 1)
+    for e in engines:
+        _lib.call("es_ctx_profile", e._h, 1)
+    step_bytes = bp.per * 2 * H * W
     for i in range(K):
-        bp.process_frames(None, motions_for(specs, Wm + i), sync=False,
-                          images_dev=imgs[Wm + i].data_ptr())
-    bp.sync()
-    stage = np.zeros(6)
-    nsteps = ctypes.c_int64()
-    _lib.call("es_ctx_stage_times", eng._h, _lib.ptr(stage), ctypes.byref(nsteps))
-    _lib.call("es_ctx_profile", eng._h, 0)
-    st_ms = stage / max(nsteps.value, 1)
+        mot = motions_for(specs, Wm + i)
+        for g, e in enumerate(engines):
+            e.step(None, mot[g * bp.per:(g + 1) * bp.per], sync=True,
+                   images_dev=imgs[Wm + i].data_ptr() + g * step_bytes)
+    st_ms = np.zeros(6)
+    for e in engines:
+        stage = np.zeros(6)
+        nsteps = ctypes.c_int64()
+        _lib.call("es_ctx_stage_times", e._h, _lib.ptr(stage), ctypes.byref(nsteps))
+        _lib.call("es_ctx_profile", e._h, 0)
+        st_ms += stage / max(nsteps.value, 1)
 
     # ---- quality (untimed): fused left maps of the last timed frame against
     # the renderer's ground truth, evaluated on the device (metrics.py)
@@ -546,20 +582,17 @@ def main():
         outs = [torch.empty((B, H, W), dtype=torch.int16, pin_memory=True) for _ in range(K)]
         sharding.barrier()
         torch.cuda.synchronize(device)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(ext):
-            e0.record()
+        e0 = start_event()
         for i in range(K):
             # public API: pinned host images in, fused KITTI maps of all B
             # sequences out, every step
             bp.process_frames(staged[i].numpy(), motions_for(specs, Wm + i), sync=False)
             bp.fused_kitti(0, out=outs[i].numpy().view(np.uint16), sync=False)
         bp.fence()   # the last export's device->host copy is inside the timed region
-        with torch.cuda.stream(ext):
-            e1.record()
+        e1s = end_events()
         bp.sync()
         torch.cuda.synchronize(device)
-        te = sharding.max_over_ranks(e0.elapsed_time(e1), device)
+        te = sharding.max_over_ranks(max(e0.elapsed_time(e) for e in e1s), device)
         e2e = {"value": frames_total / (te / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": int(B * 2 * H * W), "d2h_bytes_per_step": int(B * H * W * 2),
                "per": "rank (each GPU copies its own B sequences)"}
@@ -610,7 +643,7 @@ def main():
                               "frac": frame_bytes / (ms_max / K / 1e3) / 1e9 / peak},
         "ncu_provenance": ({"lib_sha256": ncu["lib_sha256"], "capture": ncu.get("capture")}
                            if ncu else "no ncu capture of this library build"),
-        "gpu_launches": KERNELS_PER_STEP * K,
+        "gpu_launches": kernels_per_step(2 * bp.per) * K * bp.groups,
         "quality": quality,
         "clocks": clk,
         "e2e": e2e,

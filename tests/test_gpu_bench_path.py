@@ -155,3 +155,49 @@ def test_every_batch_schedule_equals_single_sequences(B):
             for a, b in ((want.measured_left, got.measured_left), (want.fused.right, got.fused.right)):
                 assert np.array_equal(a.values, b.values) and np.array_equal(a.valid, b.valid), (B, s, k)
             assert np.array_equal(want.measured_right_var.values, got.measured_right_var.values)
+
+
+def test_grouped_batch_equals_single_context():
+    """BatchedPipeline groups (B >= 64 runs as two contexts on their own
+    streams): the same sequences through groups=2 and groups=1 give
+    identical maps -- device-pointer and host-image inputs, deferred and
+    synced steps, the KITTI export and the device metrics of every
+    sequence (per-group pointer offsets)."""
+    import torch
+    from paper_1708_06301_b200 import pipeline, scenes
+    from paper_1708_06301_b200.core import StereoRig
+    import bench
+    B, n = 6, 4
+    rig = StereoRig(f=180.0, b=0.54, cx=151.0, cy=46.0, width=310, height=94, d_max=40)
+    specs = [scenes.sequence_spec(seed=500 + s, n_frames=n, step=0.5, z_range=(4.0, 30.0))
+             for s in range(B)]
+    imgs, gts = bench.render_frames(specs, list(range(n)), "cuda:0", rig=rig, with_gt=True)
+    one = pipeline.BatchedPipeline(rig, B, groups=1)
+    two = pipeline.BatchedPipeline(rig, B, groups=2)
+    assert two.groups == 2 and len(two.engines) == 2
+    with pytest.raises(AttributeError):
+        two.engine
+    for k in range(n):
+        mot = [sp[2][k] for sp in specs]
+        one.process_frames(None, mot, sync=True, images_dev=imgs[k].data_ptr())
+        if k % 2:
+            two.process_frames(imgs[k].cpu().numpy(), mot, sync=True)
+        else:
+            two.process_frames(None, mot, sync=False, images_dev=imgs[k].data_ptr())
+    two.sync()
+    assert np.array_equal(one.fused_kitti(0), two.fused_kitti(0))
+    for s in range(B):
+        a, b = one.result(s), two.result(s)
+        for name in ("measured_left", "measured_right"):
+            assert np.array_equal(getattr(a, name).values, getattr(b, name).values), (s, name)
+        assert np.array_equal(a.fused.left.values, b.fused.left.values), s
+        assert np.array_equal(a.fused.right_var.values, b.fused.right_var.values), s
+        assert a.search_fraction_left == b.search_fraction_left
+    gt = gts[n - 1][:, 0].contiguous()
+    gv = (gt > 0).to(torch.uint8).contiguous()
+    h, w = rig.height, rig.width
+    qa = one.metrics(gt.data_ptr(), gv.data_ptr(), h * w)
+    qb = two.metrics(gt.data_ptr(), gv.data_ptr(), h * w)
+    assert [(r.rate, d) for r, d in qa] == [(r.rate, d) for r, d in qb]
+    with pytest.raises(ValueError):
+        pipeline.BatchedPipeline(rig, 5, groups=2)

@@ -93,8 +93,11 @@ def main():
     seq = [launches[i] for i in sorted(launches)]
     starts = [i for i, L in enumerate(seq) if "k_warp_zmax" in L["name"]]
     ends = [i for i, L in enumerate(seq) if "k_checks_fuse" in L["name"]]
-    s = starts[-1]
-    e = [x for x in ends if x > s][0]
+    # B >= 64 runs as two contexts (BatchedPipeline groups), each launching
+    # a whole step: the last step is the last `groups` context steps
+    groups = 2 if args.batch >= 64 and args.batch % 2 == 0 else 1
+    s = starts[-groups]
+    e = ends[-1]
     stages = defaultdict(lambda: {"dram_bytes_per_step": 0.0, "ms_serialised": 0.0,
                                   "alu_weighted": 0.0, "instructions": 0.0, "launches": 0})
     kernels = defaultdict(lambda: {"dram_bytes": 0.0, "ms": 0.0, "launches": 0})

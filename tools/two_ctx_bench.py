@@ -13,7 +13,8 @@ from paper_1708_06301_b200 import pipeline
 from paper_1708_06301_b200.core import StereoRig
 
 rig = StereoRig(**bench.RIG)
-B, K, Wm = 64, 8, 3
+B = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+K, Wm = 8, 3
 nctx = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 specs = bench.sequence_specs(B, seed0=1000)
 imgs = bench.render_frames(specs, list(range(Wm + K)), "cuda:0")

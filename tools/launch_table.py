@@ -1,5 +1,7 @@
 """Per-kernel totals of an ncu launch list (--metrics gpu__time_duration.sum --csv),
-the last timed step only (the launches after the final k_checks_fuse but one)."""
+the last timed step only.  usage: launch_table.py CSV [GROUPS]; GROUPS = the
+BatchedPipeline contexts per step (2 for the B = 64 bench), each launching a
+whole step."""
 import csv
 import sys
 from collections import defaultdict
@@ -19,8 +21,9 @@ for r in rows:
 # one step = from a k_warp_zmax_tile to the next k_checks_fuse; take the last full one
 starts = [i for i, (n, _) in enumerate(seq) if n.startswith("k_warp_zmax")]
 ends = [i for i, (n, _) in enumerate(seq) if n.startswith("k_checks_fuse")]
-s = starts[-1]
-e = [x for x in ends if x > s][0]
+groups = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+s = starts[-groups]
+e = [x for x in ends if x > starts[-1]][0]
 tot = defaultdict(float)
 for n, ms in seq[s:e + 1]:
     tot[n] += ms

@@ -76,7 +76,10 @@ struct SW {
   static constexpr int BUFW = NG * NCH * CW;    // staged words per step (upper bound)
   static constexpr int REC = 3 * G * NW + 8;    // hand-over record: A0, C0, C1 + 6 splats
 };
-constexpr int SW_WARPS = 16;   // warps per CTA = strips per round
+#ifndef SW_CTA_WARPS
+#define SW_CTA_WARPS 16
+#endif
+constexpr int SW_WARPS = SW_CTA_WARPS;   // warps per CTA = strips per round
 #ifndef SW_RS_SLOTS
 #define SW_RS_SLOTS 2
 #endif
@@ -156,7 +159,11 @@ __device__ __forceinline__ void mb_arrive(unsigned b) {
 }
 
 template <int G, int NCH, bool INIT>
+#ifdef SW_MAXREG
+__global__ void __maxnreg__(SW_MAXREG) k_sgm_sweep(SweepArgs v) {
+#else
 __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
+#endif
   using T = SW<G, NCH>;
   constexpr int NG = T::NG, CW = T::CW, NW = T::NW, PPL = SW_PPL, REC = T::REC;
   constexpr int BUFW = T::BUFW;

@@ -236,51 +236,10 @@ __device__ __forceinline__ void cost_runs_row(const CostArgs& a, int rmax) {
       if (lane >= o) incl += v;
     }
     const int excl = incl - nrun;
-    const int total = __shfl_sync(FULL, incl, 31);
     const uint32_t grun0 = __shfl_sync(FULL, run0, 0);
-    for (int j = 0; j < nrun; ++j) tab[excl + j] = (uint8_t)lane;
-    __syncwarp();
-    for (int r0 = 0; r0 < total; r0 += 32) {
-      const int r = r0 + lane;
-      const bool live = r < total;
-      const int p = live ? tab[r] : 0;
-      const int plo = __shfl_sync(FULL, lo, p);
-      const int phi = __shfl_sync(FULL, hi, p);
-      const int pex = __shfl_sync(FULL, excl, p);
-      const int px = gx + p;
-      const int dbase = (plo & ~7) + (live ? 8 * (r - pex) : 0);   // idle lanes: a valid run
-      uint32_t c[8];
-      if (px >= 1 && px <= W - 2) {
-        // interior pixel: the window's columns x-1..x+1 are unclamped, so the
-        // clamped match column of (ox, d) is the edge-replicated buffer entry
-        // x + ox + sign*d, shared by neighbouring cells
-        const uint32_t r0c = refcol[px - 1], r1c = refcol[px], r2c = refcol[px + 1];
-        const int cbase = sign < 0 ? px - 1 - (dbase + 7) : px - 1 + dbase;
-        const uint32_t* ob = othpad + PADC + cbase;
-        uint32_t o[10];
-#pragma unroll
-        for (int k = 0; k < 10; ++k) o[k] = ob[k];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          // left view: cell dbase+i uses columns cbase + 7-i .. 9-i; right
-          // view: cbase + i .. i+2
-          const int k = sign < 0 ? 7 - i : i;
-          c[i] = __vsadu4(r2c, o[k + 2]) + (__vsadu4(r1c, o[k + 1]) + __vsadu4(r0c, o[k]));
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int d = dbase + i;
-          uint32_t sad = 0;
-#pragma unroll
-          for (int ox = -1; ox <= 1; ++ox) {
-            const int xx = clampi(px + ox, 0, W - 1);
-            sad = __vsadu4(refcol[xx], othpad[PADC + clampi(xx + sign * d, 0, W - 1)]) + sad;
-          }
-          c[i] = sad;
-        }
-      }
-      // interval ends (+inf) and off-image match centres (border cost)
+    // interval ends (+inf) and off-image match centres (border cost) of one
+    // pixel's run, packed for the 16-byte store
+    auto finish = [&](int px, int plo, int phi, int dbase, uint32_t (&c)[8]) -> uint4 {
       const int xm_far = px + sign * (dbase + 7), xm_near = px + sign * dbase;
       const bool fix = dbase < plo || dbase + 7 > phi || xm_far < 0 || xm_far > W - 1 ||
                        xm_near < 0 || xm_near > W - 1;
@@ -298,9 +257,127 @@ __device__ __forceinline__ void cost_runs_row(const CostArgs& a, int rmax) {
           if ((inv >> i) & 1u) c[i] = INF16;
         }
       }
-      if (live)
-        C4[grun0 + r] = make_uint4(c[0] | (c[1] << 16), c[2] | (c[3] << 16), c[4] | (c[5] << 16),
-                                   c[6] | (c[7] << 16));
+      return make_uint4(c[0] | (c[1] << 16), c[2] | (c[3] << 16), c[4] | (c[5] << 16),
+                        c[6] | (c[7] << 16));
+    };
+
+    // ---- pairs: pixels gx+2i and gx+2i+1 over their common 8-cell blocks.
+    // Cell (x, d) sums the column SADs e(x-1, d) + e(x, d) + e(x+1, d), cell
+    // (x+1, d) e(x, d) + e(x+1, d) + e(x+2, d): the middle two are shared, so
+    // a pair run costs 4 VABSDIFF4 per two cells instead of 6.
+    const int b0 = lo >> 3, b1 = b0 + nrun - 1;       // the pixel's 8-cell blocks
+    const int pb0 = __shfl_xor_sync(FULL, b0, 1), pb1 = __shfl_xor_sync(FULL, b1, 1);
+    const int pnrun = __shfl_xor_sync(FULL, nrun, 1);
+    const int xa = gx + (lane & ~1);
+    const int cb0 = max(b0, pb0), cb1 = min(b1, pb1);
+    const bool pairable = nrun > 0 && pnrun > 0 && xa >= 1 && xa + 2 <= W - 1 && cb0 <= cb1;
+    const int npair = ((lane & 1) == 0 && pairable) ? cb1 - cb0 + 1 : 0;
+    int pincl = npair;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(FULL, pincl, o);
+      if (lane >= o) pincl += v;
+    }
+    const int pexcl = pincl - npair;
+    const int ptotal = __shfl_sync(FULL, pincl, 31);
+    for (int j = 0; j < npair; ++j) tab[pexcl + j] = (uint8_t)lane;
+    __syncwarp();
+    for (int r0 = 0; r0 < ptotal; r0 += 32) {
+      const int r = r0 + lane;
+      const bool live = r < ptotal;
+      const int p = tab[live ? r : 0];                 // idle lanes: a valid pair
+      const int pa_lo = __shfl_sync(FULL, lo, p), pa_hi = __shfl_sync(FULL, hi, p);
+      const int pb_lo = __shfl_sync(FULL, lo, p + 1), pb_hi = __shfl_sync(FULL, hi, p + 1);
+      const int pa_ex = __shfl_sync(FULL, excl, p), pb_ex = __shfl_sync(FULL, excl, p + 1);
+      const int pcb0 = __shfl_sync(FULL, cb0, p), ppex = __shfl_sync(FULL, pexcl, p);
+      const int blk = pcb0 + (live ? r - ppex : 0);
+      const int dbase = 8 * blk;
+      const int px = gx + p;
+      const uint32_t r0c = refcol[px - 1], r1c = refcol[px], r2c = refcol[px + 1],
+                     r3c = refcol[px + 2];
+      const int cbase = sign < 0 ? px - 1 - (dbase + 7) : px - 1 + dbase;
+      const uint32_t* ob = othpad + PADC + cbase;
+      uint32_t o[11];
+#pragma unroll
+      for (int k = 0; k < 11; ++k) o[k] = ob[k];
+      uint32_t ca[8], cbv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        // left view: cell dbase+i of pixel x uses columns cbase + 7-i .. 9-i,
+        // of pixel x+1 one column further; right view: cbase + i .. i+2
+        const int k = sign < 0 ? 7 - i : i;
+        const uint32_t m = __vsadu4(r2c, o[k + 2]) + __vsadu4(r1c, o[k + 1]);
+        ca[i] = __vsadu4(r0c, o[k]) + m;
+        cbv[i] = __vsadu4(r3c, o[k + 3]) + m;
+      }
+      const uint4 wa = finish(px, pa_lo, pa_hi, dbase, ca);
+      const uint4 wb = finish(px + 1, pb_lo, pb_hi, dbase, cbv);
+      if (live) {
+        C4[grun0 + pa_ex + (blk - (pa_lo >> 3))] = wa;
+        C4[grun0 + pb_ex + (blk - (pb_lo >> 3))] = wb;
+      }
+    }
+    __syncwarp();
+
+    // ---- single runs: every block of a pixel outside its pair's common
+    // range (all of them for unpaired pixels and image-edge pixels)
+    const int nl = pairable ? cb0 - b0 : nrun;           // blocks left of the common range
+    const int nsing = pairable ? nrun - (cb1 - cb0 + 1) : nrun;
+    int sincl = nsing;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(FULL, sincl, o);
+      if (lane >= o) sincl += v;
+    }
+    const int sexcl = sincl - nsing;
+    const int stotal = __shfl_sync(FULL, sincl, 31);
+    for (int j = 0; j < nsing; ++j) tab[sexcl + j] = (uint8_t)lane;
+    __syncwarp();
+    for (int r0 = 0; r0 < stotal; r0 += 32) {
+      const int r = r0 + lane;
+      const bool live = r < stotal;
+      const int p = tab[live ? r : 0];
+      const int plo = __shfl_sync(FULL, lo, p);
+      const int phi = __shfl_sync(FULL, hi, p);
+      const int pex = __shfl_sync(FULL, excl, p);
+      const int psx = __shfl_sync(FULL, sexcl, p);
+      const int pnl = __shfl_sync(FULL, nl, p);
+      const int pcb1 = __shfl_sync(FULL, cb1, p);
+      const int j = live ? r - psx : 0;
+      const int blk = j < pnl ? (plo >> 3) + j : pcb1 + 1 + (j - pnl);
+      const int dbase = 8 * blk;
+      const int px = gx + p;
+      uint32_t c[8];
+      if (px >= 1 && px <= W - 2) {
+        // interior pixel: the window's columns x-1..x+1 are unclamped, so the
+        // clamped match column of (ox, d) is the edge-replicated buffer entry
+        // x + ox + sign*d, shared by neighbouring cells
+        const uint32_t r0c = refcol[px - 1], r1c = refcol[px], r2c = refcol[px + 1];
+        const int cbase = sign < 0 ? px - 1 - (dbase + 7) : px - 1 + dbase;
+        const uint32_t* ob = othpad + PADC + cbase;
+        uint32_t o[10];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) o[k] = ob[k];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int k = sign < 0 ? 7 - i : i;
+          c[i] = __vsadu4(r2c, o[k + 2]) + (__vsadu4(r1c, o[k + 1]) + __vsadu4(r0c, o[k]));
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int d = dbase + i;
+          uint32_t sad = 0;
+#pragma unroll
+          for (int ox = -1; ox <= 1; ++ox) {
+            const int xx = clampi(px + ox, 0, W - 1);
+            sad = __vsadu4(refcol[xx], othpad[PADC + clampi(xx + sign * d, 0, W - 1)]) + sad;
+          }
+          c[i] = sad;
+        }
+      }
+      const uint4 wv = finish(px, plo, phi, dbase, c);
+      if (live) C4[grun0 + pex + (blk - (plo >> 3))] = wv;
     }
     __syncwarp();
   }

@@ -88,19 +88,23 @@ __global__ void k_warp_zmax(PredArgs a) {
 // k_warp_zmax on 32x8 pixel tiles: the tile's (32+2r)x(8+2r) neighbourhood
 // of d and valid is staged in shared memory once, so the edge test
 // (prediction.py:50-64) reads its window on chip instead of 9 global loads
-// per pixel (r <= ZT_RMAX)
+// per pixel.  The window radius R (edge_window, 0 = no edge rejection) is a
+// template parameter: the tile geometry and the window loop are compile-time
+// (a runtime radius cost integer divisions in the staging loop and a
+// rolled window walk; prediction stage 2.52 -> 2.22 ms per B = 64 step)
 constexpr int ZT_W = 32, ZT_H = 8, ZT_RMAX = 2;
 
+template <int R>
 __global__ void __launch_bounds__(ZT_W * ZT_H) k_warp_zmax_tile(PredArgs a) {
-  __shared__ double td[(ZT_H + 2 * ZT_RMAX) * (ZT_W + 2 * ZT_RMAX)];
-  __shared__ uint8_t tv[(ZT_H + 2 * ZT_RMAX) * (ZT_W + 2 * ZT_RMAX)];
+  constexpr int r = R;
+  constexpr int TW = ZT_W + 2 * r, TH = ZT_H + 2 * r;
+  __shared__ double td[TH * TW];
+  __shared__ uint8_t tv[TH * TW];
   const int sv = blockIdx.z;
   const int s = sv >> 1;
   if (!a.have_pred[s]) return;
   const int W = a.rig.W, H = a.rig.H;
   const size_t HW = (size_t)W * H;
-  const int r = a.prm.edge_reject ? a.prm.edge_window : 0;
-  const int TW = ZT_W + 2 * r, TH = ZT_H + 2 * r;
   const int bx = blockIdx.x * ZT_W, by = blockIdx.y * ZT_H;
   const double* d = a.sd + sv * HW;
   const uint8_t* v = a.sv + sv * HW;
@@ -121,10 +125,12 @@ __global__ void __launch_bounds__(ZT_W * ZT_H) k_warp_zmax_tile(PredArgs a) {
   double dp = 0.0;
   if (tv[c]) {
     bool edge = false;
-    if (a.prm.edge_reject) {
+    if (R > 0) {
       // off-image neighbours are ignored (cval = -+inf), invalid ones too
       double hi = -INFINITY, lo = INFINITY;
+#pragma unroll
       for (int oy = -r; oy <= r; ++oy)
+#pragma unroll
         for (int ox = -r; ox <= r; ++ox) {
           const int k = c + oy * TW + ox;
           if (tv[k]) {
@@ -329,9 +335,13 @@ void launch_predict(const PredArgs& a, int n_sv, cudaStream_t st) {
   dim3 grid((HW + 255) / 256, n_sv);
   cudaMemsetAsync(a.zkey, 0, sizeof(unsigned long long) * (size_t)HW * n_sv, st);
   cudaMemsetAsync(a.zidx, 0xFF, sizeof(uint32_t) * (size_t)HW * n_sv, st);
-  if (!a.prm.edge_reject || a.prm.edge_window <= ZT_RMAX) {
+  // edge_window 0 with edge rejection on keeps the generic kernel (a 1x1
+  // window still compares 0 > gamma_e)
+  if (!a.prm.edge_reject || (a.prm.edge_window >= 1 && a.prm.edge_window <= ZT_RMAX)) {
     dim3 tg((a.rig.W + ZT_W - 1) / ZT_W, (a.rig.H + ZT_H - 1) / ZT_H, n_sv);
-    k_warp_zmax_tile<<<tg, dim3(ZT_W, ZT_H), 0, st>>>(a);
+    if (!a.prm.edge_reject) k_warp_zmax_tile<0><<<tg, dim3(ZT_W, ZT_H), 0, st>>>(a);
+    else if (a.prm.edge_window == 1) k_warp_zmax_tile<1><<<tg, dim3(ZT_W, ZT_H), 0, st>>>(a);
+    else k_warp_zmax_tile<2><<<tg, dim3(ZT_W, ZT_H), 0, st>>>(a);
   } else {
     k_warp_zmax<<<grid, 256, 0, st>>>(a);
   }

@@ -621,7 +621,7 @@ def main():
         "stage_ms_per_step": {n: st_ms[i] for i, n in enumerate(stage_names)},
         "stage_timing": "second untimed replay of the same frames with per-stage CUDA events "
                         "(the headline is timed with stage events off)",
-        "roofline": {"bound": "hbm", "kernel": "sgm aggregation (k_sgm_grp4 jobs)",
+        "roofline": {"bound": "hbm", "kernel": "sgm aggregation stage (fused vertical+diagonal sweeps + row jobs, all contexts)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
                      "traffic": agg_ncu["dram_bytes_per_step"] if agg_ncu else None,

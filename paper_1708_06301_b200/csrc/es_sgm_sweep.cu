@@ -296,11 +296,24 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
       __syncwarp();
     }
 
+#ifdef SW_META_SLOW
     auto load_meta = [&](int t) -> uint2 {
       const int x = xb0 + q + t;
       if (t <= t1 && in_img(x)) return meta[(size_t)(up ? H - 1 - t : t) * W + x];
       return make_uint2(SW_NONE, 0u);
     };
+#else
+    // the lane's chain pixel at step t is meta_q[t * mstride] for t in
+    // [mlo, mhi] (x = xb0 + q + t inside the image, t <= t1): one multiply-
+    // add and a range test per step
+    const int mstride = up ? 1 - W : 1 + W;
+    const uint2* meta_q = meta + (up ? (ptrdiff_t)(H - 1) * W : 0) + (xb0 + q);
+    const int mlo = max(0, -(xb0 + q)), mhi = min(t1, W - 1 - xb0 - q);
+    auto load_meta = [&](int t) -> uint2 {
+      if (t >= mlo && t <= mhi) return meta_q[(ptrdiff_t)t * mstride];
+      return make_uint2(SW_NONE, 0u);
+    };
+#endif
     auto issue = [&](uint2 mt, int slot) -> uint32_t {
       __syncwarp();   // every lane is done reading this slot (two steps ago)
       uint32_t st = 0xFFFFFFFFu, en = 0u;

@@ -880,15 +880,35 @@ extern "C" int es_ctx_export_all(es_ctx* c, int what, int view, void* out, int s
 // ------------------------------------------------------------ stage level
 
 namespace {
+// stage-level scratch: stream-ordered allocations from the device's default
+// memory pool, which keeps up to 4 GB of freed blocks cached (release
+// threshold raised once per device), so repeated stage calls neither pay
+// cudaMalloc / cudaFree nor their implicit device synchronisations
+void keep_pool_cached() {
+  static std::mutex mu;
+  static uint64_t done = 0;   // bit per device
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done >> dev & 1) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = 4ull << 30;   // bounded: big contexts still get their memory
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done |= 1ull << dev;
+}
+
 struct Scratch {
   std::vector<void*> ptrs;
+  Scratch() { keep_pool_cached(); }
   ~Scratch() {
-    for (void* p : ptrs) cudaFree(p);
+    for (void* p : ptrs) cudaFreeAsync(p, 0);
   }
   template <class T>
   T* get(size_t n) {
     void* p = nullptr;
-    if (cudaMalloc(&p, sizeof(T) * (n ? n : 1)) != cudaSuccess) return nullptr;
+    if (cudaMallocAsync(&p, sizeof(T) * (n ? n : 1), 0) != cudaSuccess) return nullptr;
     ptrs.push_back(p);
     return (T*)p;
   }

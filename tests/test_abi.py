@@ -93,3 +93,22 @@ def test_device_calls_fail_loudly_without_gpu():
     with pytest.raises(RuntimeError):
         sgm.search_intervals(core.DisparityMap(np.zeros(rig.shape), np.zeros(rig.shape, bool)),
                              core.VarianceMap(np.zeros(rig.shape)), rig)
+
+
+def test_batched_pipeline_groups_validate_before_device_work():
+    """BatchedPipeline's context groups (B >= 64 runs as two contexts): a
+    batch that does not split raises ValueError before any device call."""
+    from paper_1708_06301_b200 import core, pipeline
+    rig = core.StereoRig(f=100.0, b=0.5, cx=15.0, cy=10.0, width=32, height=20, d_max=8)
+    with pytest.raises(ValueError, match="groups"):
+        pipeline.BatchedPipeline(rig, 5, groups=2)
+    with pytest.raises(ValueError, match="groups"):
+        pipeline.BatchedPipeline(rig, 4, groups=0)
+
+
+def test_bench_launch_count_by_path():
+    """bench.py's gpu_launches claim: 13 kernels per context step with the
+    fused sweeps (>= 64 views per context), 19 with per-direction jobs."""
+    import bench
+    assert bench.kernels_per_step(64) == 13 and bench.kernels_per_step(128) == 13
+    assert bench.kernels_per_step(32) == 19 and bench.kernels_per_step(2) == 19

@@ -183,6 +183,19 @@ bool ensure_attr(const void* kernel, cudaFuncAttribute attr, int value) {
   set[key] = value;
   return true;
 }
+int device_sms() {
+  static std::mutex mu;
+  static std::map<int, int> sms;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = sms.find(dev);
+  if (it != sms.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  sms[dev] = n;
+  return n;
+}
 }  // namespace es
 
 struct es_ctx {

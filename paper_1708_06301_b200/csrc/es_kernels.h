@@ -13,6 +13,8 @@ namespace es {
 // caller's cudaGetLastError) when the device refuses
 bool ensure_smem(const void* kernel, size_t bytes);
 bool ensure_attr(const void* kernel, cudaFuncAttribute attr, int value);
+// SM count of the current device (cached per device; 148 on a B200)
+int device_sms();
 
 // ---- prediction (es_predict.cu); all arrays are [n_sv][H][W] ------------
 struct PredArgs {

@@ -568,6 +568,9 @@ static void launch_grp3(const SgmArgs& a, int nch_pairs, int fam, int sweeps, in
 //  * no select for the first family's forward sweep: the predicated partial
 //    sum load leaves 0.
 constexpr int G4_WARPS = 4;
+#ifndef G4_PF_WORDS
+#define G4_PF_WORDS 128   // row-stream L2 prefetch distance in 32-bit words (0: off)
+#endif
 
 struct G4Step {
   int base;         // pair offset (this view) of the lane's pairs in chunk 0
@@ -671,9 +674,26 @@ __global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int
     // chain metadata: every lane loads its chain's pixel itself, four steps
     // ahead, into the register set of the step's parity (no register
     // rotation, so nothing waits on a load before its use)
+    // Row chains stream through memory: a row's allocations are packed one
+    // after the other in x order, and its metadata is one array.  Every
+    // global load of this kernel sits on one scoreboard (ptxas), so a step's
+    // first use of loaded data waits for the slowest load in flight; an L2
+    // prefetch of the stream G4_PF_WORDS ahead of the pixel being decoded
+    // (fire and forget, no scoreboard) turns those loads into L2 hits.
+    // pf: word offset up to (down to, backward sweeps) which the chain's
+    // stream has been requested, 4 lines (one per lane of the group) at a time.
+    const bool rowpf = G4_PF_WORDS > 0 && (sweeps & 4) && fam == FAM_H && G == 4;
+    int pf = -1;
     auto load_meta = [&](int t) -> uint2 {
       int x, y;
-      if (t < len && grp_pixel(fam, bwd, ch, t, W, H, x, y)) return meta[(size_t)y * W + x];
+      if (t < len && grp_pixel(fam, bwd, ch, t, W, H, x, y)) {
+        const uint2* mp = meta + (size_t)y * W + x;
+        if (rowpf && gl == 0 && (t & 15) == 0) {
+          const int t2 = t + 32;
+          if (t2 < len) asm volatile("prefetch.global.L2 [%0];" ::"l"(bwd ? mp - 32 : mp + 32));
+        }
+        return *mp;
+      }
       return make_uint2(NONE, 0u);
     };
     auto info = [&](uint2 mt) -> G4Step {
@@ -687,6 +707,30 @@ __global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int
         s.spanp = (uint32_t)(j1 - j0 + PPL);
         clo = j0 / CW;
         chi = j1 / CW;
+        if (rowpf) {
+          const int as = (int)(mt.y - ((uint32_t)j0 & 3u));   // allocation start (words)
+          if (!bwd) {
+            if (pf < 0) pf = as;
+            if (pf < as + G4_PF_WORDS) {
+              const int o = pf + 32 * gl;
+              if ((size_t)o < a.volcap) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(C + o));
+                if constexpr (load_sum) asm volatile("prefetch.global.L2 [%0];" ::"l"(S + o));
+              }
+              pf += 128;
+            }
+          } else {
+            if (pf < 0) pf = as + 128;
+            if (pf > as - G4_PF_WORDS) {
+              const int o = pf - 32 * (gl + 1);
+              if (o >= 0) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(C + o));
+                if constexpr (load_sum) asm volatile("prefetch.global.L2 [%0];" ::"l"(S + o));
+              }
+              pf -= 128;
+            }
+          }
+        }
       }
       s.um = umask(__reduce_min_sync(FULL, clo), __reduce_max_sync(FULL, chi));
       return s;
@@ -820,7 +864,10 @@ static void launch_family(const SgmArgs& a, int nch, int fam, int sweeps, int in
 
 static void launch_grp4_g(int G, const SgmArgs& a, int fam, int init, int n_sv, cudaStream_t st,
                           int sweeps = 3) {
-  if (G <= 4) launch_grp4<4, 4, 4>(a, fam, init, n_sv, st, sweeps);
+#ifndef G4_MINB
+#define G4_MINB 4
+#endif
+  if (G <= 4) launch_grp4<4, 4, G4_MINB>(a, fam, init, n_sv, st, sweeps);
   else if (G == 8) launch_grp4<8, 4, 1>(a, fam, init, n_sv, st, sweeps);
   else if (G == 16) launch_grp4<16, 4, 1>(a, fam, init, n_sv, st, sweeps);
   else launch_grp4<32, 4, 1>(a, fam, init, n_sv, st, sweeps);
@@ -887,8 +934,12 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
       const bool sweep_first = parts == 2 && ((p == 1 && order) || order == 2);
       if (sweep_first) launch_sweep(v, true, vs);
       // both regime variants of the row job on one stream
-      launch_grp4_g(4 << widen, lo, FAM_H, sweep_first ? 0 : 1, n_sv, st_lo[p], p == 0 ? 1 : 2);
-      launch_grp4_g(8 << widen, hi, FAM_H, sweep_first ? 0 : 1, n_sv, st_lo[p], p == 0 ? 1 : 2);
+      // sweeps bit 2: row-stream L2 prefetch (k_sgm_grp4), for batches that
+      // fill the GPU only -- small batches are bound by the row walk's
+      // latency and lose to its extra instructions (B = 8: 1240 vs 1396
+      // frames/s; B = 64: 1914-1924 vs 1882-1889)
+      launch_grp4_g(4 << widen, lo, FAM_H, sweep_first ? 0 : 1, n_sv, st_lo[p], (p == 0 ? 1 : 2) | 4);
+      launch_grp4_g(8 << widen, hi, FAM_H, sweep_first ? 0 : 1, n_sv, st_lo[p], (p == 0 ? 1 : 2) | 4);
       if (!sweep_first) launch_sweep(v, parts == 4, vs);
     }
     return parts;
@@ -1195,21 +1246,25 @@ __device__ __forceinline__ void wta_finish(const WtaArgs& a, const SumRows<N>& s
 constexpr int WR_WARPS = 8;
 
 template <int N, int U>
-__global__ void __launch_bounds__(WR_WARPS * 32) k_wta_runs(WtaArgs a, int rmax) {
+__global__ void __launch_bounds__(WR_WARPS * 32) k_wta_runs(WtaArgs a, int rmax, int n_sv) {
   extern __shared__ uint32_t wsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t* key = wsm + wid * 32;
   uint8_t* tab = reinterpret_cast<uint8_t*>(wsm + WR_WARPS * 32) + wid * 32 * rmax;
   const size_t HW = (size_t)a.W * a.H;
-  const int svl = blockIdx.y;
-  const uint2* meta = a.meta + (size_t)svl * HW;
-  const uint4* Sv[N];
-  Sv[0] = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(a.S) + (size_t)svl * a.volcap);
+  // work items: (view, 32-pixel group), taken in a grid-wide stride so a grid
+  // of whole waves (launch_wta_variance) ends together whatever the batch
+  const uint32_t ngroups = (uint32_t)((HW + 31) / 32);
+  const size_t nitems = (size_t)ngroups * (size_t)n_sv;
+  for (size_t it = (size_t)blockIdx.x * WR_WARPS + wid; it < nitems; it += (size_t)gridDim.x * WR_WARPS) {
+    const int svl = (int)(it / ngroups);
+    const size_t g = it - (size_t)svl * ngroups;
+    const uint2* meta = a.meta + (size_t)svl * HW;
+    const uint4* Sv[N];
+    Sv[0] = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(a.S) + (size_t)svl * a.volcap);
 #pragma unroll
-  for (int i = 1; i < N; ++i)
-    Sv[i] = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(a.Sx[i - 1]) + (size_t)svl * a.volcap);
-  const size_t ngroups = (HW + 31) / 32;
-  for (size_t g = (size_t)blockIdx.x * WR_WARPS + wid; g < ngroups; g += (size_t)gridDim.x * WR_WARPS) {
+    for (int i = 1; i < N; ++i)
+      Sv[i] = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(a.Sx[i - 1]) + (size_t)svl * a.volcap);
     const size_t pix = g * 32 + lane;
     uint2 mt = make_uint2(0u, 0u);
     int lo = 0, hi = -1, nrun = 0;
@@ -1299,13 +1354,19 @@ void launch_wta_variance(const WtaArgs& a, int n_sv, cudaStream_t st) {
     const int rmax = (npairs_max(a.d_max) + 3) / 4;
     const size_t smem = sizeof(uint32_t) * WR_WARPS * 32 + (size_t)WR_WARPS * 32 * rmax;
     const size_t groups = (HW + 31) / 32;
-    // blocks per (seq, view): enough that the whole batch fills every SM a few times
-    const unsigned per_sv = (unsigned)std::min<size_t>((groups + WR_WARPS - 1) / WR_WARPS,
-                                                       std::max<size_t>(16, (148 * 8 + n_sv - 1) / n_sv));
-    dim3 grid(per_sv, n_sv);
+    // a 1-D grid of whole waves (4 resident blocks of 8 warps per SM at 64
+    // registers) striding over (view, group) items: the round-1 grid of ~19
+    // blocks per view was 2.05 waves at 64 views, i.e. a third, nearly empty
+    // wave.  Measured at B = 64 (stage ms per step): 1 wave 4.6, 2 waves
+    // 3.7, 4 waves 3.65, 8 waves 3.47 (old grid 3.9).
+    static const int waves = getenv("ES_WTA_WAVES") ? std::max(1, atoi(getenv("ES_WTA_WAVES"))) : 8;
+    const size_t items = groups * (size_t)n_sv;
+    const unsigned nblk = (unsigned)std::min<size_t>((items + WR_WARPS - 1) / WR_WARPS,
+                                                     (size_t)device_sms() * 4 * waves);
+    dim3 grid(nblk);
     auto go = [&](auto kern) {
       ensure_smem((const void*)kern, smem);
-      kern<<<grid, WR_WARPS * 32, smem, st>>>(a, rmax);
+      kern<<<grid, WR_WARPS * 32, smem, st>>>(a, rmax, n_sv);
     };
     // runs in flight per lane: four for narrow views, two for wide ones
     // (measured: 1242 px rows 3.49 -> 3.21 ms with four; 2048 px rows 4.75 ->

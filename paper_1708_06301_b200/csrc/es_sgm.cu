@@ -833,6 +833,238 @@ __global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int
   }
 }
 
+// ------------------------------------------------------------ row chains, operands through a cp.async ring
+//
+// k_sgm_grp4's recurrence with its operand path replaced.  grp4 fetches the
+// cost / partial-sum words into registers two steps ahead, but ptxas tracks
+// every global load of that kernel on ONE scoreboard, so the first use of
+// any loaded register drains all loads in flight and the two-step lead
+// collapses (ncu: 28% of the row jobs' stall samples on a step's first
+// metadata test).  Here each lane copies its own 16-byte words of the pixel
+// RL steps ahead into a lane-private slot of a per-warp shared-memory ring
+// with cp.async (one commit group per step, cp.async.wait_group RL: a true
+// RL-step lead that no other load can shorten), reads them back with LDS at
+// use, and only the 8-byte metadata loads remain on the LDG scoreboard.
+// Words outside the pixel's interval read a 16-byte +inf pad instead of
+// their (unwritten) slot.
+#ifndef ROW_RL
+#define ROW_RL 2          // steps of lead; the ring has RL + 1 slots
+#endif
+#ifndef ROW_CTA_WARPS
+#define ROW_CTA_WARPS 4
+#endif
+#ifndef ROW_MINB
+#define ROW_MINB 4
+#endif
+constexpr int ROW_WARPS = ROW_CTA_WARPS;
+template <int NCH, bool LOAD_SUM>
+constexpr size_t row_smem() {
+  // [warp][slot][chunk][C (, S)][lane] 16-byte words + one +inf pad
+  return (size_t)ROW_WARPS * (ROW_RL + 1) * NCH * (LOAD_SUM ? 2 : 1) * 32 * 16 + 16;
+}
+
+template <int NCH, bool LOAD_SUM>
+__global__ void __launch_bounds__(ROW_WARPS * 32, ROW_MINB) k_sgm_row(SgmArgs a, int bwd, int pfon) {
+  static_assert(ROW_RL == 2, "the walk below is unrolled for a three-slot ring");
+  constexpr int G = 4, PPL = 4, NG = 32 / G, CW = PPL * G, NW = PPL * NCH;
+  constexpr int CHB = (LOAD_SUM ? 2 : 1) * 512;   // bytes per chunk of a slot (cost words, then partial-sum words)
+  constexpr int SLOTB = NCH * CHB;             // bytes per ring slot
+  constexpr int NSLOT = ROW_RL + 1;
+  constexpr uint32_t NONE = 0xFFFFFFFFu;
+  extern __shared__ __align__(16) uint8_t rsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gl = lane & (G - 1), grp = lane / G, gbase = lane & ~(G - 1);
+  const int W = a.W, H = a.H;
+  const int c0 = (blockIdx.x * ROW_WARPS + wid) * NG;
+  if (threadIdx.x < 4) reinterpret_cast<uint32_t*>(rsm + (size_t)ROW_WARPS * NSLOT * SLOTB)[threadIdx.x] = INF16x2;
+  __syncthreads();
+  if (c0 >= H) return;
+  if (a.select) {
+    const double frac = (double)a.cells[blockIdx.y] / ((double)W * H * (a.d_max + 1));
+    if ((a.select == 1) == (frac > a.split)) return;
+  }
+  const int y = c0 + grp;
+  const size_t HW = (size_t)W * H;
+  const uint32_t* __restrict__ C = reinterpret_cast<const uint32_t*>(a.C) + (size_t)blockIdx.y * a.volcap;
+  uint32_t* S = reinterpret_cast<uint32_t*>(a.S) + (size_t)blockIdx.y * a.volcap;
+  const int src_l = gbase | ((gl + G - 1) & (G - 1));
+  const int src_r = gbase | ((gl + 1) & (G - 1));
+  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(rsm) + (unsigned)(wid * NSLOT * SLOTB) + 16u * lane;
+  const unsigned inf_s = (unsigned)__cvta_generic_to_shared(rsm) + (unsigned)(ROW_WARPS * NSLOT * SLOTB);
+  // the row's metadata, walked with a running pointer (rows past the image:
+  // the lane group idles on NONE pixels)
+  const int mdir = bwd ? -1 : 1;
+  const uint2* mptr = a.meta + (size_t)blockIdx.y * HW + (size_t)min(y, H - 1) * W + (bwd ? W - 1 : 0);
+  const int mlen = y < H ? W : 0;
+  int mt_next = 0;   // step of the next metadata load
+  const bool rowpf = G4_PF_WORDS > 0 && pfon;
+  int pf = -1;
+  auto load_meta = [&]() -> uint2 {
+    uint2 m = make_uint2(NONE, 0u);
+    if (mt_next < mlen) {
+      if (rowpf && gl == 0 && (mt_next & 15) == 0 && mt_next + 32 < mlen)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(mptr + 32 * mdir));
+      m = *mptr;
+    }
+    mptr += mdir;
+    ++mt_next;
+    return m;
+  };
+  auto info = [&](uint2 mt) -> G4Step {
+    G4Step s{0, 0, 0u, 0u};
+    int clo = NCH, chi = -1;
+    if (mt.x != NONE) {
+      const int j0 = (int)((mt.x & 0xFFFFu) >> 1);
+      const int j1 = (int)((mt.x >> 16) >> 1);
+      s.base = (int)(mt.y - (uint32_t)j0) + PPL * gl;
+      s.relb = PPL * gl - j0 + PPL - 1;
+      s.spanp = (uint32_t)(j1 - j0 + PPL);
+      clo = j0 / CW;
+      chi = j1 / CW;
+      if (rowpf) {
+        // L2 prefetch of the row's packed stream ahead of this pixel, four
+        // 128-byte lines (one per lane of the group) at a time
+        const int as = (int)(mt.y - ((uint32_t)j0 & 3u));   // allocation start (words)
+        if (!bwd) {
+          if (pf < 0) pf = as;
+          if (pf < as + G4_PF_WORDS) {
+            const int o = pf + 32 * gl;
+            if ((size_t)o < a.volcap) {
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(C + o));
+              if (LOAD_SUM) asm volatile("prefetch.global.L2 [%0];" ::"l"(S + o));
+            }
+            pf += 128;
+          }
+        } else {
+          if (pf < 0) pf = as + 128;
+          if (pf > as - G4_PF_WORDS) {
+            const int o = pf - 32 * (gl + 1);
+            if (o >= 0) {
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(C + o));
+              if (LOAD_SUM) asm volatile("prefetch.global.L2 [%0];" ::"l"(S + o));
+            }
+            pf -= 128;
+          }
+        }
+      }
+    }
+    uint32_t um = 0u;
+    const int ulo = __reduce_min_sync(FULL, clo), uhi = __reduce_max_sync(FULL, chi);
+    if (uhi >= ulo) um = ((2u << uhi) - 1u) & ~((1u << ulo) - 1u);
+    s.um = um;
+    return s;
+  };
+  auto pred_of = [&](const G4Step& s, int c) -> bool { return (uint32_t)(s.relb + c * CW) < s.spanp; };
+  // the lane's words of pixel `s` into ring slot `slot` (one commit group)
+  auto issue = [&](const G4Step& s, unsigned slot) {
+#pragma unroll
+    for (int c = 0; c < NCH; ++c)
+      if ((s.um >> c) & 1u) {
+        const int p = pred_of(s, c);
+        const unsigned dst = slot + (unsigned)(c * CHB);
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q cp.async.cg.shared.global [%0], [%1], 16;\n\t}\n"
+                     ::"r"(dst), "l"(C + s.base + c * CW), "r"(p) : "memory");
+        if (LOAD_SUM)
+          asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q cp.async.cg.shared.global [%0], [%1], 16;\n\t}\n"
+                       ::"r"(dst + 512u), "l"(S + s.base + c * CW), "r"(p) : "memory");
+      }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  uint32_t prev[NW];
+#pragma unroll
+  for (int w = 0; w < NW; ++w) prev[w] = INF16x2;
+  uint32_t mp2 = INF16x2, ng = INF16x2;   // no predecessor: L = C
+  const uint32_t p1x2 = a.p1i * 0x10001u;
+  // pixel t lives in ring slot t % 3 with its decoded step in s[t % 3] and
+  // its metadata register m[t % 3]; at step t the pixel t + 2 is decoded and
+  // issued, the metadata of t + 5 requested, and pixel t computed
+  G4Step s0 = info(load_meta());
+  issue(s0, ring_s);
+  G4Step s1 = info(load_meta());
+  issue(s1, ring_s + SLOTB);
+  G4Step s2{0, 0, 0u, 0u};
+  uint2 m2 = load_meta(), m0 = load_meta(), m1 = load_meta();
+  auto step = [&](const G4Step& cur, unsigned slot_use, G4Step& nx, uint2& mreg, unsigned slot_fill) {
+    nx = info(mreg);
+    mreg = load_meta();
+    issue(nx, slot_fill);
+    asm volatile("cp.async.wait_group 2;" ::: "memory");
+    uint32_t nmin = INF16x2;
+    uint32_t left_old = INF16x2;
+    uint32_t* Sb = S + cur.base;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      uint32_t P[PPL];
+#pragma unroll
+      for (int k = 0; k < PPL; ++k) P[k] = prev[c * PPL + k];
+      if ((cur.um >> c) & 1u) {
+        const bool p = pred_of(cur, c);
+        const unsigned src = slot_use + (unsigned)(c * CHB);
+        uint32_t cn[PPL], sn[PPL];
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(cn[0]), "=r"(cn[1]), "=r"(cn[2]), "=r"(cn[3]) : "r"(p ? src : inf_s));
+        if (LOAD_SUM)
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(sn[0]), "=r"(sn[1]), "=r"(sn[2]), "=r"(sn[3]) : "r"(src + 512u));
+        const uint32_t srcl = gl == G - 1 ? left_old : P[PPL - 1];
+        const uint32_t srcr = gl == 0 ? (c + 1 < NCH ? prev[(c + 1 < NCH ? c + 1 : 0) * PPL] : INF16x2) : P[0];
+        const uint32_t pl = __shfl_sync(FULL, srcl, src_l);
+        const uint32_t pr = __shfl_sync(FULL, srcr, src_r);
+        uint32_t X[PPL + 1];
+        X[0] = __byte_perm(pl, P[0], 0x5432);
+#pragma unroll
+        for (int k = 1; k < PPL; ++k) X[k] = __byte_perm(P[k - 1], P[k], 0x5432);
+        X[PPL] = __byte_perm(P[PPL - 1], pr, 0x5432);
+        uint32_t L[PPL], Ssum[PPL];
+#pragma unroll
+        for (int k = 0; k < PPL; ++k) {
+          // L = C + min(Lp(d), Lp(d-1)+P1, Lp(d+1)+P1, m+P2) - m   (sgm.py:205-215)
+          const uint32_t cand = __viaddmin_u16x2(__vminu2(X[k], X[k + 1]), p1x2, __vminu2(P[k], mp2));
+          L[k] = __vadd2(cn[k], __vadd2(cand, ng));
+          Ssum[k] = LOAD_SUM ? __vadd2(sn[k], L[k]) : L[k];
+          prev[c * PPL + k] = L[k];
+        }
+        nmin = __vimin3_u16x2(nmin, L[0], L[1]);
+        nmin = __vimin3_u16x2(nmin, L[PPL - 2], L[PPL - 1]);
+        Vec<PPL>::st(Sb + c * CW, p, Ssum);
+      } else {
+#pragma unroll
+        for (int k = 0; k < PPL; ++k) prev[c * PPL + k] = INF16x2;
+      }
+      left_old = P[PPL - 1];
+    }
+    uint32_t hm = min(nmin & 0xFFFFu, nmin >> 16);
+#pragma unroll
+    for (int o = G / 2; o; o >>= 1) hm = min(hm, __shfl_xor_sync(FULL, hm, o));
+    const bool act = cur.spanp != 0u;
+    mp2 = act ? (hm + a.p2i) * 0x10001u : INF16x2;
+    ng = act ? ((0x10000u - hm) & 0xFFFFu) * 0x10001u : INF16x2;
+  };
+  for (int t = 0; t < W; t += 3) {
+    step(s0, ring_s, s2, m2, ring_s + 2 * SLOTB);
+    if (t + 1 >= W) break;
+    step(s1, ring_s + SLOTB, s0, m0, ring_s);
+    if (t + 2 >= W) break;
+    step(s2, ring_s + 2 * SLOTB, s1, m1, ring_s + SLOTB);
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+static void launch_row(const SgmArgs& a, int bwd, int init, int pfon, int n_sv, cudaStream_t st) {
+  const int nchains = a.H;
+  constexpr int per_block = ROW_WARPS * 8;
+  dim3 grid((nchains + per_block - 1) / per_block, n_sv);
+  const int nch = (npairs_max(a.d_max) + 15) / 16;
+  auto go = [&](auto kern, size_t smem) {
+    ensure_smem((const void*)kern, smem);
+    kern<<<grid, ROW_WARPS * 32, smem, st>>>(a, bwd, pfon);
+  };
+  if (nch <= 1) { if (init) go(k_sgm_row<1, false>, row_smem<1, false>()); else go(k_sgm_row<1, true>, row_smem<1, true>()); }
+  else if (nch <= 2) { if (init) go(k_sgm_row<2, false>, row_smem<2, false>()); else go(k_sgm_row<2, true>, row_smem<2, true>()); }
+  else { if (init) go(k_sgm_row<4, false>, row_smem<4, false>()); else go(k_sgm_row<4, true>, row_smem<4, true>()); }
+}
+
 template <int G, int PPL, int MINB>
 static void launch_grp4(const SgmArgs& a, int fam, int init, int n_sv, cudaStream_t st,
                         int sweeps = 3) {
@@ -938,7 +1170,11 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
       // fill the GPU only -- small batches are bound by the row walk's
       // latency and lose to its extra instructions (B = 8: 1240 vs 1396
       // frames/s; B = 64: 1914-1924 vs 1882-1889)
-      launch_grp4_g(4 << widen, lo, FAM_H, sweep_first ? 0 : 1, n_sv, st_lo[p], (p == 0 ? 1 : 2) | 4);
+      static const int row_env = getenv("ES_SGM_ROW") ? atoi(getenv("ES_SGM_ROW")) : 1;
+      if (row_env && widen == 0 && npairs_max(a.d_max) <= 64)
+        launch_row(lo, p, sweep_first ? 0 : 1, 1, n_sv, st_lo[p]);
+      else
+        launch_grp4_g(4 << widen, lo, FAM_H, sweep_first ? 0 : 1, n_sv, st_lo[p], (p == 0 ? 1 : 2) | 4);
       launch_grp4_g(8 << widen, hi, FAM_H, sweep_first ? 0 : 1, n_sv, st_lo[p], (p == 0 ? 1 : 2) | 4);
       if (!sweep_first) launch_sweep(v, parts == 4, vs);
     }

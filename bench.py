@@ -73,8 +73,12 @@ TEXTURE_SCALE = 0.05
 # fill_h, fill_v, cost, wta, fuse + the aggregation -- from 64 views per
 # context the two fused sweeps and the two row jobs x 2 regime variants (13),
 # below that six per-direction jobs x 2 regime variants (19)
-def kernels_per_step(views_per_context):
-    return 13 if views_per_context >= 64 else 19
+def kernels_per_step(views_per_context, shared_views=0):
+    """Launches of one context step: 13 with the fused sweeps (a context of
+    >= 64 views, or >= 32 views in a batch of >= 128 views split over several
+    contexts), 19 with the per-direction aggregation jobs."""
+    fused = views_per_context >= 64 or (views_per_context >= 32 and shared_views >= 128)
+    return 13 if fused else 19
 
 
 # Integer roofline of the aggregation (SURVEY 8(d): its arithmetic intensity
@@ -425,6 +429,9 @@ def main():
     ap.add_argument("--cpu-procs", type=int, default=default_cpu_procs())
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--groups", type=int, default=None,
+                    help="device contexts the per-GPU batch is split into (default: "
+                         "pipeline.default_groups)")
     ap.add_argument("--full-range", action="store_true",
                     help="PipelineParams(baseline=True): every frame full range (the config-1 "
                          "workload per frame; tuning aid, not the headline)")
@@ -470,8 +477,8 @@ def main():
     frames = list(range(Wm + K))
     imgs = render_frames(specs, frames, device)
     bp = pipeline.BatchedPipeline(rig, B, pipeline.PipelineParams(baseline=args.full_range),
-                                  device=local)
-    # B >= 64 runs as two contexts of B/2 on their own streams (see
+                                  device=local, groups=args.groups)
+    # B >= 64 runs as several contexts of B/groups on their own streams (see
     # BatchedPipeline): the timed regions start on an event every group's
     # stream waits for and end at the last group's completion
     engines = bp.engines
@@ -601,6 +608,14 @@ def main():
     peak, peak_kind = peaks()
     ncu = measured_ncu(args.config, B, TEXTURE_SCALE)
     nst = (ncu or {}).get("stages", {})
+    # several contexts overlap in the timed step, and the replay above runs
+    # them one after the other (a 32-view sweep then holds 64 SMs for its
+    # whole duration with the rest of the GPU idle): a stage's cost IN the
+    # step is the timed step apportioned by the stage's share of the
+    # serialised replay.  One context: the replay is the step's own order.
+    st_serial = st_ms.copy()
+    if bp.groups > 1:
+        st_ms = st_serial / st_serial.sum() * (ms_max / K)
     agg_ms = st_ms[3]
     hw = H * W
     agg_bytes = 4 * cells + 8 * hw * 2 * B
@@ -619,8 +634,13 @@ def main():
         "searched_mcells_per_s": cells * world / (ms_max / K / 1e3) / 1e6,
         "search_fraction": cells / (2 * B * hw * (D_MAX + 1)),
         "stage_ms_per_step": {n: st_ms[i] for i, n in enumerate(stage_names)},
+        "stage_ms_serialised": {n: st_serial[i] for i, n in enumerate(stage_names)},
         "stage_timing": "second untimed replay of the same frames with per-stage CUDA events "
-                        "(the headline is timed with stage events off)",
+                        "(the headline is timed with stage events off); stage_ms_serialised = "
+                        "sum over contexts of the replay's stage times (contexts one after the "
+                        "other); stage_ms_per_step = the timed step apportioned by those shares "
+                        "when several contexts overlap (equal to the replay for one context); "
+                        "the rooflines use stage_ms_per_step",
         "roofline": {"bound": "hbm", "kernel": "sgm aggregation stage (fused vertical+diagonal sweeps + row jobs, all contexts)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
@@ -643,7 +663,7 @@ def main():
                               "frac": frame_bytes / (ms_max / K / 1e3) / 1e9 / peak},
         "ncu_provenance": ({"lib_sha256": ncu["lib_sha256"], "capture": ncu.get("capture")}
                            if ncu else "no ncu capture of this library build"),
-        "gpu_launches": kernels_per_step(2 * bp.per) * K * bp.groups,
+        "gpu_launches": kernels_per_step(2 * bp.per, 2 * bp.batch if bp.groups > 1 else 0) * K * bp.groups,
         "quality": quality,
         "clocks": clk,
         "e2e": e2e,

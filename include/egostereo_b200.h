@@ -101,6 +101,13 @@ int es_ctx_have_state(es_ctx* ctx, int seq, int64_t* have);
  * summed milliseconds per stage over the recorded steps and clears them */
 int es_ctx_profile(es_ctx* ctx, int enable);
 int es_ctx_stage_times(es_ctx* ctx, double* ms6, int64_t* steps);
+/* scheduling hint for a batch split over several contexts of one device
+ * (BatchedPipeline groups): total_batch = sequences of ALL cooperating
+ * contexts.  The SGM aggregation picks its GPU-filling schedule (fused
+ * vertical+diagonal sweeps, one SM per view) when the contexts together
+ * bring at least 64 views, although this context alone would not.  Results
+ * do not depend on it.  0 (default): this context's own batch decides. */
+int es_ctx_shared_batch(es_ctx* ctx, int total_batch);
 
 /* FrameResult materialisation (pipeline.py:53-72) of the last step into
  * host memory; `what` selects the map, `view` 0 = left, 1 = right. */

@@ -65,6 +65,7 @@ SIGNATURES = {
     "es_ctx_have_state": [_P, _I, _P],
     "es_ctx_cells_acc": [_P, _P, _I],
     "es_ctx_profile": [_P, _I],
+    "es_ctx_shared_batch": [_P, _I],
     "es_ctx_stage_times": [_P, _P, _P],
     "es_ctx_export": [_P, _I, _I, _I, _P],
     "es_ctx_export_all": [_P, _I, _I, _P, _I],

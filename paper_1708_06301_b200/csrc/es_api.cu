@@ -215,6 +215,7 @@ struct es_ctx {
   uint32_t* Sx[3] = {nullptr, nullptr, nullptr};
   cudaStream_t sx[7] = {};
   int parts_live = 1;                  // partial sums holding the last step's total
+  int shared_batch = 0;                // es_ctx_shared_batch: sequences of all cooperating contexts
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   uint8_t* img = nullptr;
   double* sd[2] = {nullptr, nullptr};
@@ -616,6 +617,7 @@ int es_ctx_step(es_ctx* c, const uint8_t* images, int images_dev, const double* 
   sa.lanes = c->lanes;
   sa.cells = c->cells;
   sa.sweep_ring = c->sw_ring;
+  sa.shared_views = 2 * c->shared_batch;
   static const double split = getenv("ES_SGM_SPLIT") ? atof(getenv("ES_SGM_SPLIT")) : 0.6;
   sa.split = split;
   if (c->arith == ARITH_U16 && !c->lanes) {
@@ -722,6 +724,12 @@ int es_ctx_cells_acc(es_ctx* c, uint64_t* total, int reset) {
   CK(cudaStreamSynchronize(c->st));
   *total = v;
   if (reset) CK(cudaMemsetAsync(c->cells_acc, 0, sizeof(v), c->st));
+  return ES_OK;
+}
+
+int es_ctx_shared_batch(es_ctx* c, int total_batch) {
+  if (total_batch < 0) return fail(ES_ERR_VALUE, "total_batch must be >= 0");
+  c->shared_batch = total_batch;
   return ES_OK;
 }
 

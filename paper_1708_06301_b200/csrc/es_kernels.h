@@ -84,6 +84,8 @@ struct SgmArgs {
   // fused vertical + diagonal sweeps (launch_aggregate_parts): the
   // round-boundary hand-over buffers of the two sweeps (null: grp4 jobs only)
   uint32_t* sweep_ring = nullptr;   // [2][n_sv][sweep_ring_words]
+  // views of all contexts sharing the device with this launch (0: n_sv)
+  int shared_views = 0;
 };
 // full 8-path aggregation; the u16 path runs 4 family launches (both sweeps
 // each), the f32 path runs the 8 directions in the reference's order

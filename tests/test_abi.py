@@ -112,3 +112,7 @@ def test_bench_launch_count_by_path():
     import bench
     assert bench.kernels_per_step(64) == 13 and bench.kernels_per_step(128) == 13
     assert bench.kernels_per_step(32) == 19 and bench.kernels_per_step(2) == 19
+    # contexts of 32 views sharing a batch of >= 128 views keep the fused sweeps
+    assert bench.kernels_per_step(32, 128) == 13 and bench.kernels_per_step(16, 128) == 19
+    from paper_1708_06301_b200 import pipeline
+    assert [pipeline.default_groups(b) for b in (1, 32, 63, 64, 66, 96)] == [1, 1, 1, 4, 2, 4]

@@ -175,6 +175,7 @@ def test_grouped_batch_equals_single_context():
     one = pipeline.BatchedPipeline(rig, B, groups=1)
     two = pipeline.BatchedPipeline(rig, B, groups=2)
     assert two.groups == 2 and len(two.engines) == 2
+    three = pipeline.BatchedPipeline(rig, B, groups=3)
     with pytest.raises(AttributeError):
         two.engine
     for k in range(n):
@@ -184,8 +185,11 @@ def test_grouped_batch_equals_single_context():
             two.process_frames(imgs[k].cpu().numpy(), mot, sync=True)
         else:
             two.process_frames(None, mot, sync=False, images_dev=imgs[k].data_ptr())
+        three.process_frames(None, mot, sync=False, images_dev=imgs[k].data_ptr())
     two.sync()
+    three.sync()
     assert np.array_equal(one.fused_kitti(0), two.fused_kitti(0))
+    assert np.array_equal(one.fused_kitti(1), three.fused_kitti(1))
     for s in range(B):
         a, b = one.result(s), two.result(s)
         for name in ("measured_left", "measured_right"):

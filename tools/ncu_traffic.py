@@ -93,9 +93,10 @@ def main():
     seq = [launches[i] for i in sorted(launches)]
     starts = [i for i, L in enumerate(seq) if "k_warp_zmax" in L["name"]]
     ends = [i for i, L in enumerate(seq) if "k_checks_fuse" in L["name"]]
-    # B >= 64 runs as two contexts (BatchedPipeline groups), each launching
-    # a whole step: the last step is the last `groups` context steps
-    groups = 2 if args.batch >= 64 and args.batch % 2 == 0 else 1
+    # B >= 64 runs as several contexts (BatchedPipeline groups), each
+    # launching a whole step: the last step is the last `groups` context steps
+    from paper_1708_06301_b200.pipeline import default_groups
+    groups = default_groups(args.batch)
     s = starts[-groups]
     e = ends[-1]
     stages = defaultdict(lambda: {"dram_bytes_per_step": 0.0, "ms_serialised": 0.0,

@@ -75,9 +75,9 @@ TEXTURE_SCALE = 0.05
 # below that six per-direction jobs x 2 regime variants (19)
 def kernels_per_step(views_per_context, shared_views=0):
     """Launches of one context step: 13 with the fused sweeps (a context of
-    >= 64 views, or >= 32 views in a batch of >= 128 views split over several
+    >= 64 views, or >= 24 views in a batch of >= 48 views split over several
     contexts), 19 with the per-direction aggregation jobs."""
-    fused = views_per_context >= 64 or (views_per_context >= 32 and shared_views >= 128)
+    fused = views_per_context >= 64 or (views_per_context >= 24 and shared_views >= 48)
     return 13 if fused else 19
 
 

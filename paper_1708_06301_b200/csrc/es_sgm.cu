@@ -1131,10 +1131,13 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
   // B = 16: 1086 vs 1481 -- measured); smaller batches keep the
   // per-direction jobs (ES_SGM_SWEEP=0 / 1 force it off / on)
   static const int sweep_env = getenv("ES_SGM_SWEEP") ? atoi(getenv("ES_SGM_SWEEP")) : -1;
-  // (views of all contexts sharing the device count: four contexts of 32
-  // views pack the SMs better than two of 64 -- 2005 vs 1937 frames/s at
-  // B = 64 -- but a context below 32 views keeps the per-direction jobs)
-  const bool use_sweep = sweep_env < 0 ? (n_sv >= 64 || (n_sv >= 32 && a.shared_views >= 128)) : sweep_env > 0;
+  // (views of all contexts sharing the device count: contexts of ~32 views
+  // pack the SMs better than one large context -- B = 64: 2005 frames/s as
+  // 4 x 16 sequences vs 1937 as 2 x 32 and 1715 as one; B = 24: 1539 as
+  // 2 x 12 vs 1262 -- pipeline.default_groups; a context on its own below
+  // 64 views keeps the per-direction jobs)
+  const bool use_sweep =
+      sweep_env < 0 ? (n_sv >= 64 || (n_sv >= 24 && a.shared_views >= 48)) : sweep_env > 0;
   if (g4 && use_sweep && a.sweep_ring && (parts == 2 || parts == 4) && sweep_lanes(a.d_max)) {
     // fused vertical + diagonal sweeps (es_sgm_sweep.cu): each partial sum
     // takes one row job and one three-direction sweep: S0 = rows ->, then

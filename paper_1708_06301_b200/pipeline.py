@@ -318,24 +318,31 @@ class DisparityPipeline:
 
 
 def default_groups(batch: int) -> int:
-    """Device contexts a batch is split into (see BatchedPipeline)."""
-    if batch >= 64:
-        return 4 if batch % 4 == 0 else (2 if batch % 2 == 0 else 1)
-    return 1
+    """Device contexts a batch is split into (see BatchedPipeline): the
+    divisor of the batch whose contexts come closest to 16 sequences, none
+    below 12.  Measured on a B200 (frames/s, one context -> split): B = 24
+    1262 -> 1539 (2 x 12), B = 32 1626 -> 1776 (2 x 16; 4 x 8: 1461), B = 48
+    1460 -> 1915 (3 x 16; 2 x 24: 1896), B = 64 1715 -> 2005 (4 x 16; 2 x 32:
+    1937; 8 x 8: 1550), B = 96 1958 (6 x 16; 3 x 32: 1925), B = 128 1967
+    (8 x 16; 4 x 32: 1945)."""
+    best, score = 1, abs(batch - 16)
+    for g in range(2, batch // 12 + 1):
+        if batch % g == 0 and abs(batch // g - 16) < score:
+            best, score = g, abs(batch // g - 16)
+    return best
 
 
 class BatchedPipeline:
     """B independent sequences advanced together (config 5).
 
-    From 64 sequences up the batch runs as ``groups`` device contexts of
-    B/groups sequences (default 4, or 2 when B is not a multiple of 4), each
-    on its own streams: a step enqueues every group before any waits, so one
-    group's latency-bound SGM aggregation (one SM per view for ~9.5 ms)
-    overlaps the other groups' bandwidth-bound stages and the groups' sweeps
-    pack the SMs (measured at B = 64: 1 context 1715, 2 contexts 1937,
-    4 contexts 2005 frames/s).  Each context is told
-    the whole batch (``es_ctx_shared_batch``) so that its aggregation keeps
-    the GPU-filling schedule.  Sequences are independent, so the results are
+    From 24 sequences up the batch runs as ``groups`` device contexts of
+    about 16 sequences each (``default_groups``), every context on its own
+    streams: a step enqueues every group before any waits, so one group's
+    latency-bound SGM aggregation (the fused sweeps hold one SM per view for
+    ~9.5 ms) overlaps the other groups' bandwidth-bound stages and the
+    groups' sweeps pack the SMs.  Each context is told the whole batch
+    (``es_ctx_shared_batch``) so that its aggregation keeps the GPU-filling
+    schedule.  Sequences are independent, so the results are
     those of one context."""
 
     def __init__(self, rig: StereoRig, batch: int, params: PipelineParams | None = None,

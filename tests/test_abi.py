@@ -114,5 +114,7 @@ def test_bench_launch_count_by_path():
     assert bench.kernels_per_step(32) == 19 and bench.kernels_per_step(2) == 19
     # contexts of 32 views sharing a batch of >= 128 views keep the fused sweeps
     assert bench.kernels_per_step(32, 128) == 13 and bench.kernels_per_step(16, 128) == 19
+    assert bench.kernels_per_step(24, 48) == 13 and bench.kernels_per_step(32, 0) == 19
     from paper_1708_06301_b200 import pipeline
-    assert [pipeline.default_groups(b) for b in (1, 32, 63, 64, 66, 96)] == [1, 1, 1, 4, 2, 4]
+    assert [pipeline.default_groups(b) for b in (1, 8, 16, 20, 24, 32, 48, 63, 64, 96, 128)] == \
+        [1, 1, 1, 1, 2, 2, 3, 3, 4, 6, 8]

@@ -256,6 +256,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
   int it_all = 0;   // steps walked by this warp (mbarrier slot / phase)
   int nr = 0, nw = 0;   // hand-over records read from / written to the shared rings
   int nh = 0, nhr = 0;  // warp 0: global records staged / consumed
+  int head_seen = -1;   // warp 0, lane 0: last progress value read from the last warp
   const int rounds = (ns + SW_WARPS - 1) / SW_WARPS;
   for (int r = 0; r < rounds; ++r) {
 #ifdef SW_ROUND_BARRIER
@@ -351,9 +352,16 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
     // shared memory; the last warp of round r-1 wrote it long before
     auto stage_head = [&](int tr) {
       if (lane == 0) {
-        spin_ge(progs + SW_WARPS - 1, pbase + tr + 1);
-        __threadfence_block();
-        asm volatile("fence.proxy.async.global;" ::: "memory");
+        // the producer runs ~360 steps ahead: its progress word is read (and
+        // the fences paid) only when the last value seen does not cover tr
+        if (head_seen < pbase + tr + 1) {
+          do {
+            head_seen = progs[SW_WARPS - 1];
+            if (head_seen < pbase + tr + 1) __nanosleep(8);
+          } while (head_seen < pbase + tr + 1);
+          __threadfence_block();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         const unsigned b = headbar_s + 8u * (unsigned)(nh & 1);
         const unsigned dst = head_s + 4u * (unsigned)((nh & 1) * REC);
@@ -556,7 +564,10 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) k_sgm_sweep(SweepArgs v) {
           stg2_if(q == 1 && gl == 0, rec + 3 * G * NW + 4, c_p2, c_ng);
         }
       }
-      if (w == SW_WARPS - 1) publish(rbase + t + 1);
+      // the consumer of the global records (warp 0 of the next round) is
+      // hundreds of steps behind: progress is published every 16th step and
+      // at the end of the round
+      if (w == SW_WARPS - 1 && (t & 15) == 15) publish(rbase + t + 1);
       // ---- partial sums of the step's three directions
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {

@@ -95,6 +95,7 @@ def main():
     ends = [i for i, L in enumerate(seq) if "k_checks_fuse" in L["name"]]
     # B >= 64 runs as several contexts (BatchedPipeline groups), each
     # launching a whole step: the last step is the last `groups` context steps
+    sys.path.insert(0, ROOT)
     from paper_1708_06301_b200.pipeline import default_groups
     groups = default_groups(args.batch)
     s = starts[-groups]

@@ -569,7 +569,7 @@ static void launch_grp3(const SgmArgs& a, int nch_pairs, int fam, int sweeps, in
 //    sum load leaves 0.
 constexpr int G4_WARPS = 4;
 #ifndef G4_PF_WORDS
-#define G4_PF_WORDS 128   // row-stream L2 prefetch distance in 32-bit words (0: off)
+#define G4_PF_WORDS 128   // k_sgm_row: row-stream L2 prefetch distance in 32-bit words (0: off)
 #endif
 
 struct G4Step {
@@ -674,26 +674,9 @@ __global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int
     // chain metadata: every lane loads its chain's pixel itself, four steps
     // ahead, into the register set of the step's parity (no register
     // rotation, so nothing waits on a load before its use)
-    // Row chains stream through memory: a row's allocations are packed one
-    // after the other in x order, and its metadata is one array.  Every
-    // global load of this kernel sits on one scoreboard (ptxas), so a step's
-    // first use of loaded data waits for the slowest load in flight; an L2
-    // prefetch of the stream G4_PF_WORDS ahead of the pixel being decoded
-    // (fire and forget, no scoreboard) turns those loads into L2 hits.
-    // pf: word offset up to (down to, backward sweeps) which the chain's
-    // stream has been requested, 4 lines (one per lane of the group) at a time.
-    const bool rowpf = G4_PF_WORDS > 0 && (sweeps & 4) && fam == FAM_H && G == 4;
-    int pf = -1;
     auto load_meta = [&](int t) -> uint2 {
       int x, y;
-      if (t < len && grp_pixel(fam, bwd, ch, t, W, H, x, y)) {
-        const uint2* mp = meta + (size_t)y * W + x;
-        if (rowpf && gl == 0 && (t & 15) == 0) {
-          const int t2 = t + 32;
-          if (t2 < len) asm volatile("prefetch.global.L2 [%0];" ::"l"(bwd ? mp - 32 : mp + 32));
-        }
-        return *mp;
-      }
+      if (t < len && grp_pixel(fam, bwd, ch, t, W, H, x, y)) return meta[(size_t)y * W + x];
       return make_uint2(NONE, 0u);
     };
     auto info = [&](uint2 mt) -> G4Step {
@@ -707,30 +690,6 @@ __global__ void __launch_bounds__(G4_WARPS * 32, MINB) k_sgm_grp4(SgmArgs a, int
         s.spanp = (uint32_t)(j1 - j0 + PPL);
         clo = j0 / CW;
         chi = j1 / CW;
-        if (rowpf) {
-          const int as = (int)(mt.y - ((uint32_t)j0 & 3u));   // allocation start (words)
-          if (!bwd) {
-            if (pf < 0) pf = as;
-            if (pf < as + G4_PF_WORDS) {
-              const int o = pf + 32 * gl;
-              if ((size_t)o < a.volcap) {
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(C + o));
-                if constexpr (load_sum) asm volatile("prefetch.global.L2 [%0];" ::"l"(S + o));
-              }
-              pf += 128;
-            }
-          } else {
-            if (pf < 0) pf = as + 128;
-            if (pf > as - G4_PF_WORDS) {
-              const int o = pf - 32 * (gl + 1);
-              if (o >= 0) {
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(C + o));
-                if constexpr (load_sum) asm volatile("prefetch.global.L2 [%0];" ::"l"(S + o));
-              }
-              pf -= 128;
-            }
-          }
-        }
       }
       s.um = umask(__reduce_min_sync(FULL, clo), __reduce_max_sync(FULL, chi));
       return s;
@@ -1105,6 +1064,16 @@ static void launch_grp4_g(int G, const SgmArgs& a, int fam, int init, int n_sv, 
   else launch_grp4<32, 4, 1>(a, fam, init, n_sv, st, sweeps);
 }
 
+// the single-direction row jobs of the per-direction schedules (small
+// batches) run k_sgm_row as well (B = 8: 1397 -> 1430 frames/s, B = 16: 1480
+// -> 1489).  ES_SGM_ROW = 0: grp4 everywhere, 1: k_sgm_row in the sweep
+// schedules only, 2 (default): everywhere
+static bool row_small(int fam, int sweeps, int widen, int d_max) {
+  static const int row_env = getenv("ES_SGM_ROW") ? atoi(getenv("ES_SGM_ROW")) : 2;
+  return row_env >= 2 && fam == FAM_H && (sweeps == 1 || sweeps == 2) && widen == 0 &&
+         npairs_max(d_max) <= 64;
+}
+
 // u16 aggregation with the per-(seq, view) regime choice: views with reduced
 // intervals run the narrow variant on st_lo[p], wide ones the wide variant on
 // st_hi[p]; each (seq, view) is handled by exactly one of them, so the two
@@ -1172,16 +1141,12 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
       const bool sweep_first = parts == 2 && ((p == 1 && order) || order == 2);
       if (sweep_first) launch_sweep(v, true, vs);
       // both regime variants of the row job on one stream
-      // sweeps bit 2: row-stream L2 prefetch (k_sgm_grp4), for batches that
-      // fill the GPU only -- small batches are bound by the row walk's
-      // latency and lose to its extra instructions (B = 8: 1240 vs 1396
-      // frames/s; B = 64: 1914-1924 vs 1882-1889)
-      static const int row_env = getenv("ES_SGM_ROW") ? atoi(getenv("ES_SGM_ROW")) : 1;
+      static const int row_env = getenv("ES_SGM_ROW") ? atoi(getenv("ES_SGM_ROW")) : 2;
       if (row_env && widen == 0 && npairs_max(a.d_max) <= 64)
         launch_row(lo, p, sweep_first ? 0 : 1, 1, n_sv, st_lo[p]);
       else
-        launch_grp4_g(4 << widen, lo, FAM_H, sweep_first ? 0 : 1, n_sv, st_lo[p], (p == 0 ? 1 : 2) | 4);
-      launch_grp4_g(8 << widen, hi, FAM_H, sweep_first ? 0 : 1, n_sv, st_lo[p], (p == 0 ? 1 : 2) | 4);
+        launch_grp4_g(4 << widen, lo, FAM_H, sweep_first ? 0 : 1, n_sv, st_lo[p], p == 0 ? 1 : 2);
+      launch_grp4_g(8 << widen, hi, FAM_H, sweep_first ? 0 : 1, n_sv, st_lo[p], p == 0 ? 1 : 2);
       if (!sweep_first) launch_sweep(v, parts == 4, vs);
     }
     return parts;
@@ -1227,7 +1192,10 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
       hi.select = 2;
       lo.S = S[j.part];
       hi.S = S[j.part];
-      launch_grp4_g(4 << widen, lo, j.fam, j.init, n_sv, st_lo[j.part], j.sweeps);
+      if (row_small(j.fam, j.sweeps, widen, a.d_max))
+        launch_row(lo, j.sweeps == 2, j.init, n_sv >= 48, n_sv, st_lo[j.part]);
+      else
+        launch_grp4_g(4 << widen, lo, j.fam, j.init, n_sv, st_lo[j.part], j.sweeps);
       launch_grp4_g(8 << widen, hi, j.fam, j.init, n_sv, st_hi[j.part], j.sweeps);
     }
     return parts;
@@ -1280,7 +1248,10 @@ int launch_aggregate_parts(const SgmArgs& a, int n_sv, int parts, void* const* S
       hi.select = 2;
       lo.S = S[j.part];
       hi.S = S[j.part];
-      launch_grp4_g(4 << widen, lo, j.fam, j.init, n_sv, st_lo[j.part], j.sweeps);
+      if (row_small(j.fam, j.sweeps, widen, a.d_max))
+        launch_row(lo, j.sweeps == 2, j.init, n_sv >= 48, n_sv, st_lo[j.part]);
+      else
+        launch_grp4_g(4 << widen, lo, j.fam, j.init, n_sv, st_lo[j.part], j.sweeps);
       launch_grp4_g(8 << widen, hi, j.fam, j.init, n_sv, st_hi[j.part], j.sweeps);
     }
     return parts;

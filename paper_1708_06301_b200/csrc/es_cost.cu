@@ -157,6 +157,12 @@ __device__ __forceinline__ void cost_runs_row(const CostArgs& a, int rmax) {
   const uint2* meta = a.meta + (size_t)svl * HW + (size_t)y * W;
   const uint32_t rowbase = (uint32_t)(y * row_capacity(W, a.d_max));
   const int y0 = max(y - 1, 0), y2 = min(y + 1, H - 1);
+  // the metadata of the warp's first 32 pixels is requested before the image
+  // rows are staged (and every later group's one iteration ahead): ncu had
+  // 12% of this kernel's stall samples on the first use of a metadata word
+  // loaded at the top of its own iteration
+  uint2 mt_next = make_uint2(0u, 0u);
+  if (wid * 32 + lane < W) mt_next = meta[wid * 32 + lane];
   if (a.tma) {
     // TMA: the three rows of both images land in shared memory as byte rows
     // by six bulk copies (16-byte-aligned supersets of the rows, one elected
@@ -222,8 +228,9 @@ __device__ __forceinline__ void cost_runs_row(const CostArgs& a, int rmax) {
     const int x = gx + lane;
     int lo = 0, hi = -1, nrun = 0;
     uint32_t run0 = 0;   // row-relative run index of the pixel's allocation
+    const uint2 mt = mt_next;
+    if (x + CR_WARPS * 32 < W) mt_next = meta[x + CR_WARPS * 32];
     if (x < W) {
-      const uint2 mt = meta[x];
       lo = (int)lo_of(mt);
       hi = (int)hi_of(mt);
       run0 = (mt.y - rowbase - pad_before(lo)) >> 2;

@@ -1459,7 +1459,7 @@ __device__ __forceinline__ void wta_finish(const WtaArgs& a, const SumRows<N>& s
 constexpr int WR_WARPS = 8;
 
 template <int N, int U>
-__global__ void __launch_bounds__(WR_WARPS * 32) k_wta_runs(WtaArgs a, int rmax, int n_sv) {
+__global__ void __launch_bounds__(WR_WARPS * 32, 4) k_wta_runs(WtaArgs a, int rmax, int n_sv) {
   extern __shared__ uint32_t wsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t* key = wsm + wid * 32;
@@ -1469,21 +1469,30 @@ __global__ void __launch_bounds__(WR_WARPS * 32) k_wta_runs(WtaArgs a, int rmax,
   // of whole waves (launch_wta_variance) ends together whatever the batch
   const uint32_t ngroups = (uint32_t)((HW + 31) / 32);
   const size_t nitems = (size_t)ngroups * (size_t)n_sv;
-  for (size_t it = (size_t)blockIdx.x * WR_WARPS + wid; it < nitems; it += (size_t)gridDim.x * WR_WARPS) {
+  const size_t istride = (size_t)gridDim.x * WR_WARPS;
+  // metadata of the lane's pixel of item `it` (requested one item ahead: ncu
+  // had 11% of this kernel's stall samples on its first use)
+  auto item_meta = [&](size_t it) -> uint2 {
+    if (it >= nitems) return make_uint2(0u, 0u);
+    const size_t sv = it / ngroups;
+    const size_t px = (it - sv * ngroups) * 32 + lane;
+    return px < HW ? a.meta[sv * HW + px] : make_uint2(0u, 0u);
+  };
+  uint2 mt_next = item_meta((size_t)blockIdx.x * WR_WARPS + wid);
+  for (size_t it = (size_t)blockIdx.x * WR_WARPS + wid; it < nitems; it += istride) {
     const int svl = (int)(it / ngroups);
     const size_t g = it - (size_t)svl * ngroups;
-    const uint2* meta = a.meta + (size_t)svl * HW;
     const uint4* Sv[N];
     Sv[0] = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(a.S) + (size_t)svl * a.volcap);
 #pragma unroll
     for (int i = 1; i < N; ++i)
       Sv[i] = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(a.Sx[i - 1]) + (size_t)svl * a.volcap);
     const size_t pix = g * 32 + lane;
-    uint2 mt = make_uint2(0u, 0u);
+    const uint2 mt = mt_next;
+    mt_next = item_meta(it + istride);
     int lo = 0, hi = -1, nrun = 0;
     uint32_t run0 = 0;
     if (pix < HW) {
-      mt = meta[pix];
       lo = (int)lo_of(mt);
       hi = (int)hi_of(mt);
       run0 = (mt.y - pad_before(lo)) >> 2;

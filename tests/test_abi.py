@@ -96,7 +96,7 @@ def test_device_calls_fail_loudly_without_gpu():
 
 
 def test_batched_pipeline_groups_validate_before_device_work():
-    """BatchedPipeline's context groups (B >= 64 runs as two contexts): a
+    """BatchedPipeline's context groups (B >= 24 runs as contexts of ~16 sequences): a
     batch that does not split raises ValueError before any device call."""
     from paper_1708_06301_b200 import core, pipeline
     rig = core.StereoRig(f=100.0, b=0.5, cx=15.0, cy=10.0, width=32, height=20, d_max=8)

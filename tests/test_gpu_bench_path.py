@@ -158,7 +158,7 @@ def test_every_batch_schedule_equals_single_sequences(B):
 
 
 def test_grouped_batch_equals_single_context():
-    """BatchedPipeline groups (B >= 64 runs as two contexts on their own
+    """BatchedPipeline groups (B >= 24 runs as contexts of ~16 sequences on their own
     streams): the same sequences through groups=2 and groups=1 give
     identical maps -- device-pointer and host-image inputs, deferred and
     synced steps, the KITTI export and the device metrics of every
